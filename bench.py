@@ -1,0 +1,349 @@
+#!/usr/bin/env python3
+"""Benchmark of the Synkhronos hot path on B200 (one JSON line on stdout).
+
+Headline workload (BASELINE.json configs[1]): input-indexing gather of
+shuffled 4096-row batches from a 10M x 256 fp32 shared dataset.
+
+  value    device-timed gather throughput (CUDA events on each rank's
+           stream, max over GPUs) with the dataset resident in HBM (the
+           SharedInput's HBM mirror), one launch per step covering
+           `--batches` x 4096 rows per GPU. Algorithmic bytes per row:
+           1024 read + 1024 written + 8 index = 2056 B.
+  e2e      the same metric through the public API (Function.call with
+           indexes, row-count kernel, Sum): every step copies its u64 index
+           list host->device and reads the f64 result back.
+  roofline gather kernel: algorithmic bytes / average launch duration vs
+           the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline  the unmodified reference (oracle/_ref/ref_driver, C++20)
+           on this box's cores, bounded sample of the same workload.
+  sync_sgd C1 (784-512-10 fp32 MLP, batch 256/GPU indexed, grad all-reduce
+           mean fused with the SGD update), samples/s through Trainer.
+
+`--impl reference` times only the reference CPU implementation on the same
+config and prints its line. Under torchrun (N>1) the synkpar executor is one
+process driving all N GPUs (the paper's master + workers model): rank 0 owns
+the pool; other ranks wait at a gloo barrier.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sync-SGD samples/s at 1/2/4/8 B200; gather/reduce GB/s vs HBM & NVLink peak"
+BYTES_PER_ROW_EXTRA = 8  # u64 index
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--rows", type=int, default=10_000_000)
+    p.add_argument("--cols", type=int, default=256)
+    p.add_argument("--batch", type=int, default=4096)
+    p.add_argument("--batches", type=int, default=64, help="4096-row batches gathered per launch (per step)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-sgd", action="store_true")
+    return p.parse_args()
+
+
+def measured_peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= self.gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
+        return rank, world, dist
+    return rank, world, None
+
+
+def run_reference_driver(mode, extra, timeout=1800):
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(exe):
+        return None, "oracle/_ref/ref_driver not built"
+    out = subprocess.run([exe, "--mode", mode, *map(str, extra)], capture_output=True, text=True, timeout=timeout)
+    if out.returncode != 0:
+        return None, out.stderr.strip()[-300:]
+    return json.loads(out.stdout.strip().splitlines()[-1]), None
+
+
+def reference_arm(args, n_gpus):
+    cores = os.cpu_count() or 1
+    rows_per_step = args.batch * args.batches * n_gpus
+    steps = max(1, args.steps)
+    res, err = run_reference_driver("gather", ["--rows", args.rows, "--cols", args.cols, "--batch", rows_per_step,
+                                               "--steps", steps, "--warmup", max(1, min(args.warmup, 3)),
+                                               "--workers", cores])
+    line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "higher_is_better": True, "n_gpus": n_gpus,
+            "steps": steps, "warmup": args.warmup, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, n_gpus)}
+    if res is None:
+        line["unavailable"] = err
+        return line
+    line.update({"value": res["gbs"], "ms_per_step": res["ms_per_step"],
+                 "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
+                                  "sample": "%d steps x %d rows gathered through call(indexes) with a no-op kernel "
+                                            "from a %dx%d f32 SharedInputArray" % (steps, rows_per_step, args.rows,
+                                                                                    args.cols)},
+                 "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    return line
+
+
+def workload_config(args, n_gpus):
+    return {"workload": "indexed gather: shuffled %d-row batches from a %dx%d fp32 shared dataset" % (
+        args.batch, args.rows, args.cols), "batches_per_step_per_gpu": args.batches,
+        "rows_per_step": args.batch * args.batches * n_gpus, "row_bytes": args.cols * 4,
+        "parallelism": "dp%d (one rank per GPU, single-process executor)" % n_gpus,
+        "l2": "inputs larger than L2 (10.24 GB dataset, 2 rotating 256 MiB outputs per GPU)"}
+
+
+def fill_dataset(sk, rows, cols):
+    arr = sk.SharedInput.alloc([rows, cols], "f32")
+    rng = np.random.default_rng(7)
+    block = 1 << 18
+    for r0 in range(0, rows, block):
+        n = min(block, rows - r0)
+        arr.write(r0, r0 + n, rng.random((n, cols), dtype=np.float32) * 2 - 1)
+    return arr
+
+
+def ours(args, n_gpus):
+    import paper_1710_04162_b200 as sk
+
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1710_04162_b200", "_lib", "libsynk_cuda.so"))
+    lib.synk_last_error.restype = ctypes.c_char_p
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+
+    def ok(rc, what):
+        if rc != 0:
+            raise RuntimeError("%s: %s" % (what, lib.synk_last_error().decode()))
+
+    rows, cols, B = args.rows, args.cols, args.batch
+    row_bytes = cols * 4
+    n_step = B * args.batches  # rows per GPU per step
+    peak, peak_kind = measured_peak_hbm()
+
+    t_setup = time.time()
+    arr = fill_dataset(sk, rows, cols)
+    pool = sk.Pool(workers=n_gpus, devices=list(range(n_gpus)))
+    arr.mirror(pool)
+    setup_s = time.time() - t_setup
+
+    handles = [vp(pool.device_handle(r)) for r in range(n_gpus)]
+    rng = np.random.default_rng(11)
+    total_steps = args.warmup + args.steps
+    idx_dev, dst_dev, mirrors = [], [], []
+    for r in range(n_gpus):
+        h = handles[r]
+        idx = rng.integers(0, rows, total_steps * n_step).astype(np.uint64)
+        p = vp()
+        ok(lib.synk_alloc(h, u64(idx.nbytes), ctypes.byref(p)), "alloc idx")
+        ok(lib.synk_copy(h, p, idx.ctypes.data_as(vp), u64(idx.nbytes)), "H2D idx")
+        idx_dev.append(p.value)
+        outs = []
+        for _ in range(2):
+            q = vp()
+            ok(lib.synk_alloc(h, u64(n_step * row_bytes), ctypes.byref(q)), "alloc out")
+            outs.append(q.value)
+        dst_dev.append(outs)
+        mirrors.append(arr.mirror_ptr(pool.device_of(r)))
+        ok(lib.synk_sync(h), "sync")
+
+    def gather_launches(step_rows, steps, warm, per_launch_marks=True):
+        """Launch `steps` gathers of step_rows rows per GPU; return (max over GPUs of
+        the device time of the timed region, mean per-launch kernel time)."""
+        marks = [[] for _ in range(n_gpus)]
+        for r in range(n_gpus):
+            ok(lib.synk_mark_reset(handles[r]), "marks")
+        for s in range(warm + steps):
+            for r in range(n_gpus):
+                h = handles[r]
+                m = ctypes.c_int()
+                if s >= warm:
+                    ok(lib.synk_mark(h, ctypes.byref(m)), "mark")
+                    marks[r].append(m.value)
+                ok(lib.synk_gather_rows(h, vp(mirrors[r]), u64(rows), u64(row_bytes),
+                                        vp(idx_dev[r] + (s * step_rows % (total_steps * n_step - step_rows + 1)) * 8),
+                                        u64(step_rows), vp(dst_dev[r][s % 2])), "gather")
+                if s >= warm:
+                    ok(lib.synk_mark(h, ctypes.byref(m)), "mark")
+                    marks[r].append(m.value)
+        region, launch = [], []
+        for r in range(n_gpus):
+            ok(lib.synk_sync(handles[r]), "sync")
+            sec = ctypes.c_double()
+            ok(lib.synk_mark_elapsed(handles[r], marks[r][0], marks[r][-1], ctypes.byref(sec)), "elapsed")
+            region.append(sec.value)
+            tot = 0.0
+            for a, b in zip(marks[r][0::2], marks[r][1::2]):
+                ok(lib.synk_mark_elapsed(handles[r], a, b, ctypes.byref(sec)), "elapsed")
+                tot += sec.value
+            launch.append(tot / steps)
+        return max(region), float(np.mean(launch))
+
+    with ClockSampler(n_gpus) as clocks:
+        region_s, launch_s = gather_launches(n_step, args.steps, args.warmup)
+    bytes_step = n_gpus * n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA)
+    value = bytes_step * args.steps / region_s / 1e9
+    achieved = n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA) / launch_s / 1e9
+    # latency of a single 4096-row batch (the per-call granularity of the config)
+    _, single_s = gather_launches(B, 50, 5)
+
+    # ---- e2e through the public API --------------------------------------------------
+    f = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
+    sk.distribute(pool)
+    e2e_idx = [rng.integers(0, rows, n_step * n_gpus) for _ in range(total_steps)]
+    for s in range(args.warmup):
+        (cnt,) = f.call([arr], indexes=e2e_idx[s])
+        assert float(cnt) == n_step * n_gpus
+    t0 = time.perf_counter()
+    for s in range(args.warmup, total_steps):
+        (cnt,) = f.call([arr], indexes=e2e_idx[s])
+    e2e_s = time.perf_counter() - t0
+    assert float(cnt) == n_step * n_gpus
+    e2e = bytes_step * args.steps / e2e_s / 1e9
+
+    # ---- sync SGD (C1) sub-measurement ------------------------------------------------
+    sgd = None
+    if not args.no_sgd:
+        cfg = sk.MlpConfig(in_dim=784, width=512, out_dim=10, layers=2, seed=1)
+        x, y = sk.mlp_make_dataset(65536, cfg, seed=2, dtype="f32")
+        sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
+        sx.mirror(pool)
+        sy.mirror(pool)
+        block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+        g = sk.mlp_grad_function(pool, block)
+        sk.distribute(pool)
+        tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
+        sel = [rng.integers(0, 65536, 256 * n_gpus) for _ in range(total_steps)]
+        for s in range(args.warmup):
+            tr.train_step(g, [sx, sy], indexes=sel[s])
+        t0 = time.perf_counter()
+        for s in range(args.warmup, total_steps):
+            loss = tr.train_step(g, [sx, sy], indexes=sel[s])
+        dt = time.perf_counter() - t0
+        rep = tr.last_report
+        sgd = {"config": "C1: MLP 784-512-10 fp32, batch 256 per GPU (scaled), indexed from a 65536-row SharedInput "
+                         "(HBM mirror), SGD lr 0.01, grad all-reduce mean fused with the update",
+               "samples_per_s": 256 * n_gpus * args.steps / dt, "ms_per_step": 1e3 * dt / args.steps,
+               "allreduce_ms_last": 1e3 * rep["allreduce_s"], "loss_last": loss, "coherent": block.params.coherent}
+
+    pool.shutdown()
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * region_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, n_gpus),
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 8 * n_step * n_gpus,
+                    "d2h_bytes_per_step": 8, "path": "Function.call(indexes) -> row_count kernel -> Sum"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
+            "single_batch_us": 1e6 * single_s,
+            "gpu_launches": n_gpus * args.steps, "clocks": clocks.summary(), "setup_s": setup_s}
+    if sgd:
+        line["sync_sgd"] = sgd
+    return line
+
+
+def main():
+    args = parse()
+    rank, world, dist = dist_setup()
+    n_gpus = max(args.gpus, world)
+    line = None
+    if rank == 0:
+        if args.impl == "reference":
+            line = reference_arm(args, n_gpus)
+        else:
+            line = ours(args, n_gpus)
+            if not args.no_cpu_baseline:
+                cores = os.cpu_count() or 1
+                res, err = run_reference_driver("gather", ["--rows", args.rows, "--cols", args.cols, "--batch",
+                                                           args.batch * args.batches, "--steps", 5, "--warmup", 1,
+                                                           "--workers", cores])
+                line["cpu_baseline"] = (
+                    {"value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
+                     "sample": "5 steps x %d rows via the unmodified reference call(indexes), no-op kernel, from the "
+                               "same %dx%d f32 dataset shape" % (args.batch * args.batches, args.rows, args.cols)}
+                    if res else {"value": None, "unavailable": err})
+    if dist is not None:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

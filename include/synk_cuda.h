@@ -1,0 +1,199 @@
+/*
+ * synk_cuda.h — C-ABI of the B200 (sm_100a) device layer behind the synkpar
+ * API. Plain pointers, sizes and int status codes; no C++ or torch types.
+ *
+ * The C++ executor (paper_1710_04162_b200/csrc/host, the drop-in for the
+ * reference's C++ sources in src/) is the only in-tree caller; INTEGRATION.md shows the
+ * ctypes binding a maintainer of the reference would add. Each entry point
+ * names the reference routine whose per-call work it replaces
+ * (file:line under /root/reference/proj).
+ *
+ * Conventions
+ *  - Every function returns 0 (SYNK_OK) or a negative SYNK_E* code; the
+ *    message is in synk_last_error() (thread-local).
+ *  - A synk_dev is one RANK: a device id, a non-blocking CUDA stream and a
+ *    stream-ordered memory pool. Rank-scoped calls are asynchronous on that
+ *    stream; synk_sync() is the phase-exit barrier (stream sync + deferred
+ *    device-side error flags, e.g. an out-of-range gather index).
+ *  - Several ranks may share one GPU (each has its own stream).
+ *  - Collectives are issued by EVERY rank of a world from its own host thread
+ *    inside one phase, after every rank's inputs are complete (the executor's
+ *    phase barrier guarantees that). Rank r only touches chunk r of every
+ *    replica, so ranks never race; replicas on other GPUs are reached by
+ *    NVLink peer loads/stores (peer access is enabled by synk_open).
+ *  - dtype codes = synkpar::DType (tensor.hpp:16-19): 1 f32, 2 f64.
+ *  - op codes = synkpar::ReduceOp order (tensor.hpp:27-34):
+ *      0 sum, 1 mean, 2 max, 3 min, 4 prod, 5 gather.
+ *  - Pointers may be device pointers or pinned, mapped host pointers
+ *    (unified addressing); synk_ptr_kind() tells which.
+ */
+#ifndef SYNK_CUDA_H
+#define SYNK_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SYNK_OK 0
+#define SYNK_EBOUNDS (-1) /* synkpar::BoundsError   */
+#define SYNK_ESHAPE (-2)  /* synkpar::ShapeError    */
+#define SYNK_EDTYPE (-3)  /* synkpar::DTypeError    */
+#define SYNK_EARG (-4)    /* synkpar::ArgumentError */
+#define SYNK_ECUDA (-10)  /* CUDA runtime failure   */
+#define SYNK_ENOMEM (-11) /* allocation failure     */
+#define SYNK_ENODEV (-12) /* no usable CUDA device  */
+
+#define SYNK_F32 1
+#define SYNK_F64 2
+
+#define SYNK_OP_SUM 0
+#define SYNK_OP_MEAN 1
+#define SYNK_OP_MAX 2
+#define SYNK_OP_MIN 3
+#define SYNK_OP_PROD 4
+#define SYNK_OP_GATHER 5
+
+/* optimizer rules, sgd.hpp:24-45 order */
+#define SYNK_RULE_SGD 0
+#define SYNK_RULE_MOMENTUM 1
+#define SYNK_RULE_RMSPROP 2
+#define SYNK_RULE_ADAM 3
+
+typedef struct synk_dev synk_dev;
+
+/* ---- runtime --------------------------------------------------------------- */
+const char* synk_last_error(void);
+int synk_abi_version(void);
+int synk_device_count(int* count);
+
+/* Open `world` rank contexts; rank r runs on device_ids[r]. Enables peer
+ * access between every pair of distinct devices. Replaces the rank bring-up
+ * of WorkerPool::fork (worker_pool.cpp:225-259). */
+int synk_open(int world, const int* device_ids, synk_dev** out);
+int synk_close(synk_dev* dev);
+int synk_dev_rank(const synk_dev* dev);
+int synk_dev_device(const synk_dev* dev);
+void* synk_dev_stream(const synk_dev* dev);
+/* Make `dev`'s device current on the calling host thread. */
+int synk_bind(const synk_dev* dev);
+/* Phase-exit barrier: stream sync + device error flags (worker_pool.cpp:58-90). */
+int synk_sync(synk_dev* dev);
+
+/* Stream-ordered timing marks (CUDA events) for CallReport/PhaseReport:
+ * synk_mark records an event on the rank's stream and returns its id;
+ * synk_mark_elapsed reads the seconds between two marks (after synk_sync);
+ * synk_mark_reset recycles every mark of the rank. */
+int synk_mark(synk_dev* dev, int* mark);
+int synk_mark_elapsed(synk_dev* dev, int a, int b, double* seconds);
+int synk_mark_reset(synk_dev* dev);
+
+/* ---- memory ------------------------------------------------------------------ */
+/* Stream-ordered HBM allocation on the rank's device (NdBuffer::allocate,
+ * tensor.cpp:32-36, for replicas and per-rank batches). */
+int synk_alloc(synk_dev* dev, uint64_t bytes, void** out);
+int synk_free(synk_dev* dev, void* ptr);
+/* Pinned, mapped, portable host memory (the SharedInputArray store,
+ * shared_input.cpp:38-64, readable by every GPU over PCIe). */
+int synk_host_alloc(uint64_t bytes, void** out);
+int synk_host_free(void* ptr);
+/* 0 = pageable host, 1 = pinned/mapped host, 2 = device memory. */
+int synk_ptr_kind(const void* ptr, int* kind, int* device);
+/* Asynchronous copy in any direction (NdBuffer::clone, tensor.cpp:155-159). */
+int synk_copy(synk_dev* dev, void* dst, const void* src, uint64_t bytes);
+/* Strided 2-D copy: `rows` rows of `row_bytes`, pitches in bytes. */
+int synk_copy2d(synk_dev* dev, void* dst, uint64_t dpitch, const void* src, uint64_t spitch,
+                uint64_t row_bytes, uint64_t rows);
+int synk_memset(synk_dev* dev, void* dst, int value, uint64_t bytes);
+/* Fill n elements with a value (NdBuffer::fill, tensor.cpp:141-151). */
+int synk_fill(synk_dev* dev, int dtype, void* dst, double value, uint64_t n);
+
+/* dst = (dst dtype) src, elementwise (NdBuffer::get/set conversions). */
+int synk_cast(synk_dev* dev, int dst_dtype, void* dst, int src_dtype, const void* src, uint64_t n);
+
+/* ---- input indexing ------------------------------------------------------------ */
+/* dst[j,:] = src[idx[j],:] for j < n_idx (gather_rows, tensor.cpp:200-217;
+ * excerpt_rows, tensor.cpp:399-409). src is HBM or pinned host; idx is u64 in
+ * HBM or pinned host. Bit-exact; an out-of-range index raises SYNK_EBOUNDS at
+ * the next synk_sync(). */
+int synk_gather_rows(synk_dev* dev, const void* src, uint64_t src_rows, uint64_t row_bytes,
+                     const uint64_t* idx, uint64_t n_idx, void* dst);
+
+/* ---- aggregation --------------------------------------------------------------- */
+/* acc = op(acc, other), op in {sum,max,min,prod}, in T (combine_inplace,
+ * tensor.cpp:250-270; max is b>a?b:a, accumulator wins ties/NaN). */
+int synk_combine(synk_dev* dev, int dtype, int op, void* acc, const void* other, uint64_t n);
+/* acc = T((f64 acc*wa + f64 other*wb) * (1/(wa+wb))) (tensor.cpp:272-285). */
+int synk_weighted_mean(synk_dev* dev, int dtype, void* acc, double wa, const void* other,
+                       double wb, uint64_t n);
+/* v = T(f64 v * factor) (scale_inplace, tensor.cpp:367-373). */
+int synk_scale(synk_dev* dev, int dtype, void* buf, double factor, uint64_t n);
+/* out = left fold of parts[0..count) in order (OutputAccumulator + the master
+ * rank fold, function.cpp:76-115,515-527). Mean is row-weighted by weights[].
+ * parts may live on peer GPUs. */
+int synk_left_fold(synk_dev* dev, int dtype, int op, void* out, const void* const* parts,
+                   const uint64_t* weights, uint32_t count, uint64_t n);
+/* Column statistics of a row-major [rows x cols] slice in one HBM pass:
+ * sum (deterministic tree order), max, min (acceptance_main.cpp:86-133 kernels).
+ * Any of the three outputs may be NULL. */
+int synk_column_stats(synk_dev* dev, int dtype, const void* x, uint64_t rows, uint64_t cols,
+                      void* sum_out, void* max_out, void* min_out);
+/* *equal = 1 iff the byte ranges match (equals_bitwise, tensor.cpp:169-173);
+ * b may be on a peer GPU. Synchronous. */
+int synk_equal(synk_dev* dev, const void* a, const void* b, uint64_t bytes, int* equal);
+/* *finite = 1 iff no NaN/Inf (all_finite, sgd.cpp:171-185). Synchronous. */
+int synk_all_finite(synk_dev* dev, int dtype, const void* x, uint64_t n, int* finite);
+
+/* ---- collectives (single process, peer memory, reference tree order) -------------- */
+/* Called by every rank r of `world` inside one phase. bufs[q] = rank q's
+ * replica (n elements). Rank r folds chunk r of all replicas in the fixed
+ * binomial order of tree_fold (replicated.cpp:16-29) and stores the result
+ * into chunk r of every replica: bitwise equal to ReplicatedVariable::
+ * all_reduce (replicated.cpp:124-137). */
+int synk_all_reduce(synk_dev* dev, int world, int dtype, int op, void* const* bufs, uint64_t n);
+/* Fold of all replicas into `out` (tree order), run by one rank
+ * (ReplicatedVariable::reduce, replicated.cpp:139-149). */
+int synk_tree_reduce(synk_dev* dev, int world, int dtype, int op, const void* const* bufs,
+                     uint64_t n, void* out);
+/* Rank r copies chunk r of bufs[src] into every other replica
+ * (ReplicatedVariable::broadcast, replicated.cpp:115-122). */
+int synk_broadcast(synk_dev* dev, int world, int src, void* const* bufs, uint64_t bytes);
+
+/* ---- optimizer ---------------------------------------------------------------- */
+/* hyper: momentum {mu}; rmsprop {rho, eps}; adam {beta1, beta2, eps}.
+ * t = post-increment step counter. f64 math, cast on store (sgd.cpp:46-88). */
+int synk_optimizer_step(synk_dev* dev, int dtype, int rule, const double* hyper, double lr,
+                        uint64_t t, void* params, const void* grads, void* aux0, void* aux1,
+                        uint64_t n);
+/* Fused gradient all-reduce + update, called by every rank of a world in one
+ * phase (SyncSgd::train_step all_reduce + step, sgd.cpp:313-319): rank r
+ * tree-folds chunk r of all gradient replicas (grad_op sum or mean),
+ * writes the reduced chunk back to every gradient replica, applies the rule
+ * to chunk r of its own params/aux and stores the new chunk into every
+ * params/aux replica. aux0/aux1 may be NULL for rules without state.
+ * replicas_coherent = 1 promises that params/aux replicas are bitwise equal
+ * (the executor tracks this), so chunk r is computed once from rank r's
+ * replica; with 0 every replica's chunk is updated from its own values,
+ * exactly as per-rank steps would (sgd.cpp:226-248). */
+int synk_all_reduce_step(synk_dev* dev, int world, int dtype, int grad_op, int rule,
+                         const double* hyper, double lr, uint64_t t, void* const* params,
+                         void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
+                         int replicas_coherent);
+
+/* ---- example function: tanh MLP loss + gradient (mlp.cpp:134-218) ---------------- */
+/* dims[0..layers]; params flat [W0 b0 W1 b1 ...]; x [n x dims0]; y [n x dims_L].
+ * Writes the f64 loss scalar to loss_dev (device) and the flat gradient (dtype)
+ * to grad. workspace from synk_mlp_workspace_bytes. */
+int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, uint64_t n,
+                             uint64_t* bytes);
+int synk_mlp_loss_grad(synk_dev* dev, int dtype, const uint64_t* dims, uint32_t layers,
+                       const void* params, const void* x, const void* y, uint64_t n,
+                       double* loss_dev, void* grad, void* workspace, uint64_t workspace_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SYNK_CUDA_H */

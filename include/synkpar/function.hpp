@@ -1,0 +1,177 @@
+#pragma once
+// Parallel functions: build -> distribute -> call (drop-in for the
+// reference's function.hpp). A call scatters explicit inputs by leading
+// dimension (optionally through a row selection), runs the kernel on every
+// rank over num_slices sequential sub-shards, aggregates outputs in place,
+// defers replica updates to one application per rank, and folds the ranks'
+// outputs in rank order on the master.
+//
+// B200 execution: rank r's share is assembled in HBM of GPU r (an indexed
+// gather kernel for index lists, a DMA or an HBM-mirror view for row
+// ranges), kernels with a `device_fn` run on rank r's stream, slice and
+// rank aggregation are device kernels (include/synk_cuda.h), and only the
+// final outputs cross back to the host. Kernels with only a host `fn`
+// (e.g. Python kernels) are still accepted: their inputs/outputs are staged
+// through host memory around the call (compatibility path).
+
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <string>
+#include <variant>
+#include <vector>
+
+#include "synkpar/device.hpp"
+#include "synkpar/replicated.hpp"
+#include "synkpar/shared_input.hpp"
+#include "synkpar/tensor.hpp"
+#include "synkpar/worker_pool.hpp"
+
+namespace synkpar {
+
+namespace detail {
+struct FunctionCore;
+}
+
+enum class InputMode { Scatter, Broadcast };
+struct InputSpec {
+    InputMode mode = InputMode::Scatter;
+};
+struct OutputSpec {
+    ReduceOp reduce = ReduceOp::Sum;
+};
+
+enum class UpdateCombine { Add, WeightedMeanByRows, Overwrite };
+const char* update_combine_name(UpdateCombine c) noexcept;
+
+struct UpdateSpec {
+    ReplicatedVariable var;
+    UpdateCombine combine = UpdateCombine::Add;
+};
+
+struct UpdateDelta {
+    std::uint64_t var_id = 0;
+    NdBuffer delta;
+    UpdateCombine combine = UpdateCombine::Add;
+};
+
+struct KernelContext {
+    std::size_t rank = 0;
+    std::size_t world = 1;
+    std::size_t slice = 0;
+    std::size_t num_slices = 1;
+    std::size_t shard_rows = 0;
+    // Host copies of the pre-call `reads` replicas (host-kernel path only).
+    const std::vector<NdBuffer>* replicas = nullptr;
+    const NdBuffer& replica(std::size_t i) const;
+
+    // ---- B200 additions (appended) ----
+    int device = -1;                          // CUDA device of this rank
+    synk_dev* dev = nullptr;                  // C-ABI rank handle (stream, pool)
+    std::shared_ptr<detail::RankDevice> rank_device;
+    // Pre-call `reads` replicas in HBM (device-kernel path).
+    const std::vector<DevBuffer>* device_replicas = nullptr;
+    const DevBuffer& device_replica(std::size_t i) const;
+    DevBuffer device_alloc(std::vector<std::size_t> shape, DType dtype) const;
+};
+
+struct KernelResult {
+    std::vector<NdBuffer> outputs;
+    std::vector<UpdateDelta> updates;
+};
+using KernelFn = std::function<KernelResult(const std::vector<NdBuffer>& inputs, const KernelContext& ctx)>;
+
+// Device-side kernel contract: inputs are this rank's HBM shards, work is
+// enqueued on ctx.dev's stream, outputs/deltas are HBM buffers of the rank.
+struct DeviceUpdateDelta {
+    std::uint64_t var_id = 0;
+    DevBuffer delta;
+    UpdateCombine combine = UpdateCombine::Add;
+};
+struct DeviceKernelResult {
+    std::vector<DevBuffer> outputs;
+    std::vector<DeviceUpdateDelta> updates;
+};
+using DeviceKernelFn =
+    std::function<DeviceKernelResult(const std::vector<DevBuffer>& inputs, const KernelContext& ctx)>;
+
+struct Kernel {
+    std::string name;
+    std::size_t arity = 0;
+    std::vector<ReplicatedVariable> reads;
+    KernelFn fn;
+    // ---- B200 addition: preferred when set ----
+    DeviceKernelFn device_fn;
+};
+
+struct CallOptions {
+    std::size_t num_slices = 1;
+    std::optional<IndexSelection> indexes;
+    std::optional<std::vector<IndexSelection>> replica_indexes;
+};
+
+struct CallReport {
+    std::vector<double> rank_compute_s;
+    std::vector<std::size_t> rank_rows;
+    double scatter_s = 0.0;
+    double reduce_s = 0.0;
+    double straggler_s = 0.0;
+    double total_s = 0.0;
+    double compute_mean_s() const noexcept;
+};
+
+struct CallResult {
+    std::vector<NdBuffer> outputs;
+    CallReport report;
+};
+
+class FunctionArg {
+public:
+    FunctionArg(NdBuffer buf) : value_(std::move(buf)) {}
+    FunctionArg(SharedInputArray arr) : value_(std::move(arr)) {}
+    FunctionArg(ReplicatedVariable var) : value_(std::move(var)) {}
+    const std::variant<NdBuffer, SharedInputArray, ReplicatedVariable>& value() const { return value_; }
+
+private:
+    std::variant<NdBuffer, SharedInputArray, ReplicatedVariable> value_;
+};
+
+class ParallelFunction {
+public:
+    ParallelFunction() = default;
+
+    std::uint64_t id() const;
+    const std::string& name() const;
+    std::size_t arity() const;
+    bool distributed() const;
+    bool valid() const noexcept { return core_ != nullptr; }
+    std::optional<UpdateCombine> update_combine_for(std::uint64_t var_id) const;
+
+    CallResult call(const std::vector<FunctionArg>& args, const CallOptions& opts = {}) const;
+    std::vector<NdBuffer> call_serial(const std::vector<FunctionArg>& args,
+                                      const std::optional<IndexSelection>& indexes = std::nullopt) const;
+
+private:
+    friend ParallelFunction function(WorkerPool&, Kernel, std::vector<InputSpec>, std::vector<OutputSpec>,
+                                     std::vector<UpdateSpec>);
+    friend void distribute(WorkerPool&);
+    explicit ParallelFunction(std::shared_ptr<detail::FunctionCore> core) : core_(std::move(core)) {}
+    std::shared_ptr<detail::FunctionCore> core_;
+};
+
+ParallelFunction function(WorkerPool& pool, Kernel kernel, std::vector<InputSpec> inputs,
+                          std::vector<OutputSpec> outputs, std::vector<UpdateSpec> updates = {});
+void distribute(WorkerPool& pool);
+
+// ---- B200 built-in device kernels (the payloads of the benchmark configs) ----
+// "identity": output 0 = the shard itself (Gather it for zero-copy concat).
+Kernel identity_kernel(std::string name = "identity");
+// "row_count": output 0 = f64 scalar rows of the shard (a no-op payload that
+// isolates input indexing, for Sum reduce).
+Kernel row_count_kernel(std::string name = "row_count");
+// "column_stats": outputs column sum, column max, and the shard itself, for
+// (Sum, Max, Gather) -- the slicing/aggregation config of the benchmark.
+Kernel column_stats_kernel(std::string name = "column_stats");
+
+} // namespace synkpar

@@ -1,0 +1,84 @@
+// Shared plumbing for the sm_100a device layer (libsynk_cuda.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "synk_cuda.h"
+
+// One rank: device + stream + per-rank device flags. Opaque in the C-ABI.
+struct synk_dev {
+    int rank = 0;
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    int* flags_dev = nullptr;   // [0] bounds error, [1] scratch result
+    int* flags_host = nullptr;  // pinned mirror for synchronous checks
+    std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
+    int marks_used = 0;
+};
+
+namespace synk {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t err, const char* what);
+
+#define SYNK_CU(call)                                                   \
+    do {                                                                \
+        cudaError_t synk_e_ = (call);                                   \
+        if (synk_e_ != cudaSuccess) return ::synk::cuda_fail(synk_e_, #call); \
+    } while (0)
+
+#define SYNK_LAUNCHED(what)                                             \
+    do {                                                                \
+        cudaError_t synk_e_ = cudaGetLastError();                       \
+        if (synk_e_ != cudaSuccess) return ::synk::cuda_fail(synk_e_, what); \
+    } while (0)
+
+#define SYNK_REQUIRE(cond, code, msg)                                   \
+    do {                                                                \
+        if (!(cond)) return ::synk::fail((code), (msg));                \
+    } while (0)
+
+// Device-side guard binding the rank's device for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+inline bool valid_dtype(int dt) { return dt == SYNK_F32 || dt == SYNK_F64; }
+inline size_t dtype_bytes(int dt) { return dt == SYNK_F32 ? 4 : 8; }
+
+// Grid for a grid-stride elementwise kernel: enough CTAs to fill every SM a
+// few times, never more than the work needs.
+inline unsigned grid_for(const synk_dev* d, uint64_t work_items, unsigned block,
+                         unsigned waves = 4) {
+    uint64_t need = (work_items + block - 1) / block;
+    uint64_t cap = (uint64_t)d->num_sms * waves;
+    if (need < 1) need = 1;
+    return (unsigned)(need < cap ? need : cap);
+}
+
+// ---- reference combine semantics (tensor.cpp:250-270) ----------------------
+template <class T>
+__device__ __forceinline__ T combine_op(int op, T a, T b) {
+    switch (op) {
+    case SYNK_OP_SUM: return a + b;
+    case SYNK_OP_MAX: return b > a ? b : a;
+    case SYNK_OP_MIN: return b < a ? b : a;
+    default: return a * b;  // SYNK_OP_PROD
+    }
+}
+
+}  // namespace synk

@@ -1,0 +1,237 @@
+// Rank contexts, memory and copies for the synkpar device layer.
+//
+// A rank = (device, non-blocking stream). HBM comes from the device's default
+// stream-ordered memory pool with an unlimited release threshold, so the
+// per-call batches/accumulators of ParallelFunction::call are recycled
+// without cudaMalloc/cudaFree on the hot path.
+
+#include <stdio.h>
+
+#include <mutex>
+#include <set>
+
+#include "common.cuh"
+
+namespace synk {
+
+static thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t err, const char* what) {
+    int code = err == cudaErrorMemoryAllocation ? SYNK_ENOMEM
+             : (err == cudaErrorNoDevice || err == cudaErrorInsufficientDriver) ? SYNK_ENODEV
+             : SYNK_ECUDA;
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(code, std::string(what) + ": " + cudaGetErrorString(err));
+}
+
+static std::mutex g_pool_mutex;
+static std::set<int> g_pools_configured;
+
+static int configure_pool(int device) {
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    if (g_pools_configured.count(device)) return SYNK_OK;
+    cudaMemPool_t pool;
+    SYNK_CU(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    SYNK_CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    g_pools_configured.insert(device);
+    return SYNK_OK;
+}
+
+}  // namespace synk
+
+using namespace synk;
+
+extern "C" {
+
+const char* synk_last_error(void) { return g_last_error.c_str(); }
+
+int synk_abi_version(void) { return 1; }
+
+int synk_device_count(int* count) {
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return SYNK_OK;
+}
+
+int synk_open(int world, const int* device_ids, synk_dev** out) {
+    SYNK_REQUIRE(world >= 1, SYNK_EARG, "synk_open: world must be >= 1");
+    int ndev = 0;
+    int rc = synk_device_count(&ndev);
+    if (rc != SYNK_OK) return rc;
+    SYNK_REQUIRE(ndev > 0, SYNK_ENODEV, "synk_open: no CUDA device visible");
+    for (int r = 0; r < world; ++r) {
+        SYNK_REQUIRE(device_ids[r] >= 0 && device_ids[r] < ndev, SYNK_EARG,
+                     "synk_open: device id out of range");
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    // Peer access between every pair of distinct devices in the world.
+    std::set<int> devs(device_ids, device_ids + world);
+    for (int a : devs) {
+        SYNK_CU(cudaSetDevice(a));
+        if (int rc2 = configure_pool(a); rc2 != SYNK_OK) return rc2;
+        for (int b : devs) {
+            if (a == b) continue;
+            int can = 0;
+            SYNK_CU(cudaDeviceCanAccessPeer(&can, a, b));
+            SYNK_REQUIRE(can, SYNK_ENODEV, "synk_open: GPUs lack peer access");
+            cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        }
+    }
+    for (int r = 0; r < world; ++r) {
+        synk_dev* d = new synk_dev();
+        d->rank = r;
+        d->device = device_ids[r];
+        SYNK_CU(cudaSetDevice(d->device));
+        SYNK_CU(cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, d->device));
+        SYNK_CU(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        SYNK_CU(cudaMalloc(&d->flags_dev, 4 * sizeof(int)));
+        SYNK_CU(cudaMemset(d->flags_dev, 0, 4 * sizeof(int)));
+        SYNK_CU(cudaHostAlloc(&d->flags_host, 4 * sizeof(int), cudaHostAllocPortable));
+        out[r] = d;
+    }
+    cudaSetDevice(prev);
+    return SYNK_OK;
+}
+
+int synk_close(synk_dev* d) {
+    if (!d) return SYNK_OK;
+    DeviceGuard g(d->device);
+    cudaStreamSynchronize(d->stream);
+    cudaStreamDestroy(d->stream);
+    cudaFree(d->flags_dev);
+    cudaFreeHost(d->flags_host);
+    for (cudaEvent_t e : d->marks) cudaEventDestroy(e);
+    delete d;
+    return SYNK_OK;
+}
+
+int synk_dev_rank(const synk_dev* d) { return d->rank; }
+int synk_dev_device(const synk_dev* d) { return d->device; }
+void* synk_dev_stream(const synk_dev* d) { return (void*)d->stream; }
+
+int synk_bind(const synk_dev* d) {
+    SYNK_CU(cudaSetDevice(d->device));
+    return SYNK_OK;
+}
+
+int synk_sync(synk_dev* d) {
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaMemcpyAsync(d->flags_host, d->flags_dev, sizeof(int), cudaMemcpyDeviceToHost,
+                            d->stream));
+    SYNK_CU(cudaStreamSynchronize(d->stream));
+    if (d->flags_host[0] != 0) {
+        cudaMemsetAsync(d->flags_dev, 0, sizeof(int), d->stream);
+        cudaStreamSynchronize(d->stream);
+        return fail(SYNK_EBOUNDS, "gather_rows(): index out of range (device check)");
+    }
+    return SYNK_OK;
+}
+
+int synk_mark(synk_dev* d, int* mark) {
+    DeviceGuard g(d->device);
+    if (d->marks_used == (int)d->marks.size()) {
+        cudaEvent_t e;
+        SYNK_CU(cudaEventCreate(&e));
+        d->marks.push_back(e);
+    }
+    *mark = d->marks_used++;
+    SYNK_CU(cudaEventRecord(d->marks[*mark], d->stream));
+    return SYNK_OK;
+}
+
+int synk_mark_elapsed(synk_dev* d, int a, int b, double* seconds) {
+    SYNK_REQUIRE(a >= 0 && b >= 0 && a < d->marks_used && b < d->marks_used, SYNK_EARG, "synk_mark_elapsed: bad mark");
+    float ms = 0.f;
+    SYNK_CU(cudaEventElapsedTime(&ms, d->marks[a], d->marks[b]));
+    *seconds = ms * 1e-3;
+    return SYNK_OK;
+}
+
+int synk_mark_reset(synk_dev* d) {
+    d->marks_used = 0;
+    return SYNK_OK;
+}
+
+int synk_alloc(synk_dev* d, uint64_t bytes, void** out) {
+    *out = nullptr;
+    if (bytes == 0) return SYNK_OK;
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaMallocAsync(out, bytes, d->stream));
+    return SYNK_OK;
+}
+
+int synk_free(synk_dev* d, void* p) {
+    if (!p) return SYNK_OK;
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaFreeAsync(p, d->stream));
+    return SYNK_OK;
+}
+
+int synk_host_alloc(uint64_t bytes, void** out) {
+    *out = nullptr;
+    if (bytes == 0) return SYNK_OK;
+    SYNK_CU(cudaHostAlloc(out, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    return SYNK_OK;
+}
+
+int synk_host_free(void* p) {
+    if (!p) return SYNK_OK;
+    SYNK_CU(cudaFreeHost(p));
+    return SYNK_OK;
+}
+
+int synk_ptr_kind(const void* p, int* kind, int* device) {
+    *kind = 0;
+    *device = -1;
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return SYNK_OK;  // unknown to CUDA: pageable host memory
+    }
+    if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+        *kind = 2;
+        *device = attr.device;
+    } else if (attr.type == cudaMemoryTypeHost) {
+        *kind = 1;
+    }
+    return SYNK_OK;
+}
+
+int synk_copy(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
+    if (bytes == 0) return SYNK_OK;
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, d->stream));
+    return SYNK_OK;
+}
+
+int synk_copy2d(synk_dev* d, void* dst, uint64_t dpitch, const void* src, uint64_t spitch,
+                uint64_t row_bytes, uint64_t rows) {
+    if (rows == 0 || row_bytes == 0) return SYNK_OK;
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDefault,
+                              d->stream));
+    return SYNK_OK;
+}
+
+int synk_memset(synk_dev* d, void* dst, int value, uint64_t bytes) {
+    if (bytes == 0) return SYNK_OK;
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaMemsetAsync(dst, value, bytes, d->stream));
+    return SYNK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+#pragma once
+// Executor internals shared by the host translation units (not installed).
+
+#include <atomic>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "synk_cuda.h"
+#include "synkpar/device.hpp"
+#include "synkpar/worker_pool.hpp"
+
+namespace synkpar::detail {
+
+struct FunctionCore;
+struct PoolState;
+
+// Map a C-ABI status to the matching synkpar exception (throws on failure).
+void check(int rc, const char* what);
+[[noreturn]] void throw_status(int rc, const std::string& what);
+
+// One rank's device context; closes the stream when the last owner drops it
+// (DevBuffers keep their rank alive, so get_value works after shutdown).
+struct RankDevice {
+    synk_dev* h = nullptr;
+    std::size_t rank = 0;
+    int device = 0;
+    ~RankDevice();
+};
+
+struct DevStorage {
+    void* ptr = nullptr;
+    std::size_t bytes = 0;
+    std::shared_ptr<RankDevice> owner;
+    ~DevStorage();
+};
+
+// Device helpers (all asynchronous on the owner's stream unless noted).
+DevBuffer dev_from_host(const std::shared_ptr<RankDevice>& rd, const NdBuffer& host);
+NdBuffer dev_to_host(const DevBuffer& buf);                    // synchronous
+void dev_to_host_into(const DevBuffer& buf, std::byte* dst);   // async on owner stream
+DevBuffer dev_clone(const std::shared_ptr<RankDevice>& rd, const DevBuffer& src);
+void dev_sync(const std::shared_ptr<RankDevice>& rd);
+int synk_dtype(DType dt);
+int synk_op(ReduceOp op);
+
+// Lazily opened context on GPU 0 for host-buffer API helpers (step_*, mlp_loss_grad).
+std::shared_ptr<RankDevice> utility_device();
+
+struct VarRecord {
+    std::uint64_t id = 0;
+    std::shared_ptr<PoolState> pool;
+    std::vector<DevBuffer> replicas;
+    // True while every replica is known bitwise equal (set by replicate /
+    // broadcast / all_reduce / the fused trainer step, cleared by any
+    // per-rank mutation). Lets the fused step compute each chunk once.
+    bool coherent = true;
+};
+
+enum class PoolLifecycle : int { Idle = 0, InPhase = 1, ShutDown = 2 };
+
+struct PoolState {
+    std::size_t world = 1;
+    bool pin_threads = false;
+    std::uint64_t session_id = 0;
+    std::atomic<std::size_t> pin_failures{0};
+    std::atomic<int> lifecycle{static_cast<int>(PoolLifecycle::Idle)};
+
+    // Phase protocol: the master publishes (task, kind) and bumps `phase_seq`;
+    // each rank runs its share and decrements `pending`; the rank that brings
+    // it to zero publishes the phase id in `done_seq`.
+    std::atomic<std::uint64_t> phase_seq{0};
+    std::atomic<std::uint64_t> done_seq{0};
+    std::atomic<std::size_t> pending{0};
+    std::atomic<int> kind{0};
+    const std::function<void(std::size_t)>* task = nullptr;
+    std::vector<std::exception_ptr> rank_errors;
+    std::vector<double> rank_seconds;
+
+    std::vector<std::thread> threads;
+    std::function<void(const std::string&)> debug_sink;
+    std::vector<std::weak_ptr<FunctionCore>> built_functions;
+
+    // B200: rank r's GPU context.
+    std::vector<std::shared_ptr<RankDevice>> ranks;
+    std::vector<synk_dev*> handles;
+};
+
+PhaseReport run_pool_phase(PoolState& st, PhaseKind kind, const std::function<void(std::size_t)>& work);
+void shutdown_pool(PoolState& st);
+void require_idle(const PoolState& st, const char* what);
+
+} // namespace synkpar::detail

@@ -1,0 +1,178 @@
+// The example MLP workload (mlp.hpp): seeded init and dataset on the host
+// (identical libstdc++ draws to the reference, so identical bytes), loss and
+// gradient on the GPU through synk_mlp_loss_grad.
+
+#include "synkpar/mlp.hpp"
+
+#include <cmath>
+#include <random>
+
+#include "internal.hpp"
+
+namespace synkpar {
+
+namespace {
+
+void validate(const MlpConfig& c) {
+    if (c.layers == 0) throw ArgumentError("mlp: layers must be >= 1");
+    if (c.in_dim == 0 || c.out_dim == 0 || (c.layers > 1 && c.width == 0))
+        throw ArgumentError("mlp: dimensions must be positive");
+}
+
+// Layer widths d[0..L] from the (weight, bias) segment pairs (mlp.cpp:84-110 rules).
+std::vector<std::uint64_t> layer_dims(const std::vector<FlatSegment>& segs) {
+    if (segs.empty() || segs.size() % 2)
+        throw ArgumentError("mlp_loss_grad: segments must alternate weight/bias pairs");
+    const std::size_t L = segs.size() / 2;
+    std::vector<std::uint64_t> d(L + 1);
+    for (std::size_t l = 0; l < L; ++l) {
+        const auto& w = segs[2 * l].shape;
+        const auto& b = segs[2 * l + 1].shape;
+        if (w.size() != 2 || b.size() != 1 || b[0] != w[1])
+            throw ArgumentError("mlp_loss_grad: segment " + std::to_string(2 * l) + " is not a (weight, bias) pair");
+        if (l == 0) d[0] = w[0];
+        else if (w[0] != d[l]) throw ShapeError("mlp_loss_grad: layer " + std::to_string(l) + " input dim does not chain");
+        d[l + 1] = w[1];
+    }
+    return d;
+}
+
+struct Checked {
+    std::vector<std::uint64_t> dims;
+    std::size_t n = 0;
+};
+
+template <class Buf>
+Checked check_operands(const Buf& params, const std::vector<FlatSegment>& segs, const Buf& x, const Buf& y) {
+    if (params.rank() != 1) throw ShapeError("mlp_loss_grad: flat_params must be rank 1");
+    if (x.rank() != 2 || y.rank() != 2) throw ShapeError("mlp_loss_grad: x and y must be rank 2");
+    if (x.shape()[0] != y.shape()[0])
+        throw ShapeError("mlp_loss_grad: x rows " + std::to_string(x.shape()[0]) + " != y rows " +
+                         std::to_string(y.shape()[0]));
+    Checked c;
+    c.dims = layer_dims(segs);
+    std::size_t expected = 0;
+    for (const FlatSegment& s : segs) expected += element_count(s.shape);
+    if (params.size() != expected) throw ShapeError("mlp_loss_grad: flat_params length does not match segments");
+    if (x.shape()[1] != c.dims.front()) throw ShapeError("mlp_loss_grad: x columns != input dim");
+    if (y.shape()[1] != c.dims.back()) throw ShapeError("mlp_loss_grad: y columns != output dim");
+    c.n = x.shape()[0];
+    if (c.n == 0) throw ArgumentError("mlp_loss_grad: empty batch");
+    return c;
+}
+
+// x/y in the parameter dtype on the device (the reference widens everything
+// to f64, so mixed dtypes are legal; we narrow/widen on the GPU).
+DevBuffer as_dtype(const std::shared_ptr<detail::RankDevice>& rd, const DevBuffer& b, DType dt) {
+    if (b.dtype() == dt) return b;
+    DevBuffer out = DevBuffer::alloc(rd, b.shape(), dt);
+    detail::check(synk_cast(rd->h, detail::synk_dtype(dt), out.data(), detail::synk_dtype(b.dtype()), b.data(), b.size()),
+                  "mlp: cast inputs");
+    return out;
+}
+
+// Enqueue loss + gradient on rd's stream. Returns (loss f64 scalar, grad).
+std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::RankDevice>& rd, const Checked& c,
+                                                 const DevBuffer& params, const DevBuffer& x, const DevBuffer& y) {
+    const DType dt = params.dtype();
+    DevBuffer xd = as_dtype(rd, x, dt), yd = as_dtype(rd, y, dt);
+    const std::uint32_t L = static_cast<std::uint32_t>(c.dims.size() - 1);
+    std::uint64_t ws_bytes = 0;
+    detail::check(synk_mlp_workspace_bytes(detail::synk_dtype(dt), c.dims.data(), L, c.n, &ws_bytes), "mlp workspace");
+    DevBuffer ws = DevBuffer::alloc(rd, {(ws_bytes + 7) / 8}, DType::Float64);
+    DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
+    DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
+    detail::check(synk_mlp_loss_grad(rd->h, detail::synk_dtype(dt), c.dims.data(), L, params.data(), xd.data(), yd.data(),
+                                     c.n, static_cast<double*>(loss.data()), grad.data(), ws.data(), ws_bytes),
+                  "mlp_loss_grad");
+    return {loss, grad};
+}
+
+} // namespace
+
+std::vector<std::vector<std::size_t>> mlp_param_shapes(const MlpConfig& c) {
+    validate(c);
+    std::vector<std::vector<std::size_t>> shapes;
+    for (std::size_t l = 0; l < c.layers; ++l) {
+        const std::size_t fan_in = l == 0 ? c.in_dim : c.width;
+        const std::size_t fan_out = l + 1 == c.layers ? c.out_dim : c.width;
+        shapes.push_back({fan_in, fan_out});
+        shapes.push_back({fan_out});
+    }
+    return shapes;
+}
+
+std::vector<NdBuffer> mlp_init_params(const MlpConfig& c, DType dtype) {
+    const auto shapes = mlp_param_shapes(c);
+    std::mt19937_64 gen(c.seed);
+    std::vector<NdBuffer> out;
+    for (std::size_t i = 0; i < shapes.size(); i += 2) {
+        std::normal_distribution<double> normal(0.0, 1.0 / std::sqrt(double(shapes[i][0])));
+        NdBuffer w = NdBuffer::zeros(shapes[i], dtype);
+        for (std::size_t j = 0; j < w.size(); ++j) w.set(j, normal(gen));
+        out.push_back(std::move(w));
+        out.push_back(NdBuffer::zeros(shapes[i + 1], dtype));
+    }
+    return out;
+}
+
+Dataset mlp_make_dataset(std::size_t rows, const MlpConfig& c, std::uint64_t seed, DType dtype) {
+    validate(c);
+    std::mt19937_64 gen(seed ^ 0x9e3779b97f4a7c15ull);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    const double scale = 1.0 / std::sqrt(double(c.in_dim));
+    std::vector<double> teacher(c.in_dim * c.out_dim);
+    for (double& t : teacher) t = normal(gen) * scale;
+    Dataset ds{NdBuffer::zeros({rows, c.in_dim}, dtype), NdBuffer::zeros({rows, c.out_dim}, dtype)};
+    std::vector<double> xr(c.in_dim);
+    for (std::size_t i = 0; i < rows; ++i) {
+        for (std::size_t j = 0; j < c.in_dim; ++j) {
+            xr[j] = normal(gen);
+            ds.x.set(i * c.in_dim + j, xr[j]);
+        }
+        for (std::size_t k = 0; k < c.out_dim; ++k) {
+            double acc = 0.0;
+            for (std::size_t j = 0; j < c.in_dim; ++j) acc += xr[j] * teacher[j * c.out_dim + k];
+            ds.y.set(i * c.out_dim + k, acc);
+        }
+    }
+    return ds;
+}
+
+LossGrad mlp_loss_grad(const NdBuffer& params, const std::vector<FlatSegment>& segs, const NdBuffer& x, const NdBuffer& y) {
+    Checked c = check_operands(params, segs, x, y);
+    auto rd = detail::utility_device();
+    DevBuffer p = detail::dev_from_host(rd, params);
+    DevBuffer xd = detail::dev_from_host(rd, x);
+    DevBuffer yd = detail::dev_from_host(rd, y);
+    auto [loss, grad] = device_loss_grad(rd, c, p, xd, yd);
+    LossGrad out;
+    out.grad = detail::dev_to_host(grad);
+    out.loss = detail::dev_to_host(loss).get(0);
+    return out;
+}
+
+Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name) {
+    Kernel k;
+    k.name = std::move(name);
+    k.arity = 2;
+    k.reads = {block.params};
+    const std::vector<FlatSegment> segs = block.segments;
+    const std::uint64_t grads_id = block.grads.id();
+    k.device_fn = [segs, grads_id](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
+        const DevBuffer& params = ctx.device_replica(0);
+        Checked c = check_operands(params, segs, in[0], in[1]);
+        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1]);
+        DeviceKernelResult r;
+        r.outputs.push_back(loss);
+        r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
+        return r;
+    };
+    return k;
+}
+
+std::vector<UpdateSpec> mlp_grad_updates(const FlatParamBlock& block) {
+    return {UpdateSpec{block.grads, UpdateCombine::WeightedMeanByRows}};
+}
+
+} // namespace synkpar

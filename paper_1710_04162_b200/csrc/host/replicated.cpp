@@ -1,0 +1,272 @@
+// Replicated variables: replica r in HBM of rank r's GPU; collectives are
+// one phase of the peer-memory tree-order kernels (include/synk_cuda.h).
+
+#include "synkpar/replicated.hpp"
+
+#include <atomic>
+#include <cstring>
+
+#include "internal.hpp"
+#include "transfer.hpp"
+
+namespace synkpar {
+
+namespace detail {
+
+
+std::vector<DevBuffer>& replicas_of(const ReplicatedVariable& var) {
+    if (!var.rec_) throw ArgumentError("empty replicated-variable handle");
+    return var.rec_->replicas;
+}
+
+std::shared_ptr<PoolState> pool_of(const ReplicatedVariable& var) {
+    if (!var.rec_) throw ArgumentError("empty replicated-variable handle");
+    return var.rec_->pool;
+}
+
+VarRecord& record_of(const ReplicatedVariable& var) {
+    if (!var.rec_) throw ArgumentError("empty replicated-variable handle");
+    return *var.rec_;
+}
+
+} // namespace detail
+
+namespace {
+
+std::atomic<std::uint64_t> g_next_var{1};
+
+detail::VarRecord& live(const std::shared_ptr<detail::VarRecord>& rec, const char* what) {
+    if (!rec) throw ArgumentError(std::string(what) + ": empty replicated-variable handle");
+    return *rec;
+}
+
+void check_rank(const detail::VarRecord& rec, std::size_t rank, const char* what) {
+    if (rank >= rec.replicas.size())
+        throw ArgumentError(std::string(what) + ": rank " + std::to_string(rank) + " out of " +
+                            std::to_string(rec.replicas.size()));
+}
+
+void check_same_shapes(const detail::VarRecord& rec, const char* what) {
+    for (std::size_t r = 1; r < rec.replicas.size(); ++r)
+        if (!rec.replicas[r].same_shape(rec.replicas[0]))
+            throw ShapeError(std::string(what) + ": replica shapes differ across ranks (" +
+                             rec.replicas[0].shape_string() + " vs rank " + std::to_string(r) + " " +
+                             rec.replicas[r].shape_string() + ")");
+}
+
+void no_phase(const detail::VarRecord& rec, const char* what) {
+    if (static_cast<detail::PoolLifecycle>(rec.pool->lifecycle.load()) == detail::PoolLifecycle::InPhase)
+        throw LifecycleError(std::string(what) + ": not allowed while a phase is in flight");
+}
+
+void not_gather(ReduceOp op, const char* what) {
+    if (op == ReduceOp::Gather) throw ArgumentError(std::string(what) + ": Gather is not a reduction (use gather())");
+}
+
+std::vector<void*> replica_ptrs(const detail::VarRecord& rec) {
+    std::vector<void*> p;
+    for (const DevBuffer& b : rec.replicas) p.push_back(b.data());
+    return p;
+}
+
+// Inside a phase: the dtype check combine_inplace performs on each fold
+// (tensor.cpp:227-240) raises there, so it surfaces as PhaseError.
+void require_same_dtype(const detail::VarRecord& rec) {
+    for (const DevBuffer& b : rec.replicas)
+        if (b.dtype() != rec.replicas[0].dtype()) throw DTypeError("combine_inplace: dtype mismatch across replicas");
+}
+
+} // namespace
+
+ReplicatedVariable replicate(WorkerPool& pool, const NdBuffer& init) {
+    auto st = detail::state_of(pool);
+    detail::require_idle(*st, "replicate");
+    auto rec = std::make_shared<detail::VarRecord>();
+    rec->id = g_next_var.fetch_add(1);
+    rec->pool = st;
+    rec->replicas.resize(st->world);
+    detail::run_pool_phase(*st, PhaseKind::Distribute, [&](std::size_t r) {
+        rec->replicas[r] = detail::dev_from_host(st->ranks[r], init);
+        detail::dev_sync(st->ranks[r]);
+    });
+    return ReplicatedVariable(std::move(rec));
+}
+
+std::uint64_t ReplicatedVariable::id() const { return live(rec_, "id").id; }
+std::size_t ReplicatedVariable::world() const { return live(rec_, "world").replicas.size(); }
+DType ReplicatedVariable::dtype() const { return live(rec_, "dtype").replicas.at(0).dtype(); }
+
+void ReplicatedVariable::broadcast(std::size_t src) {
+    detail::VarRecord& rec = live(rec_, "broadcast");
+    check_rank(rec, src, "broadcast");
+    detail::PoolState& st = *rec.pool;
+    detail::require_idle(st, "broadcast");
+    const DevBuffer& s = rec.replicas[src];
+    // Every destination gets storage of the source's shape first (a clone in
+    // the reference, replicated.cpp:118-121).
+    for (std::size_t r = 0; r < rec.replicas.size(); ++r) {
+        if (r == src) continue;
+        DevBuffer& d = rec.replicas[r];
+        if (!d.same_shape(s) || d.dtype() != s.dtype() || d.shares_storage(s) || !d.has_storage()) {
+            d = DevBuffer::alloc(st.ranks[r], s.shape(), s.dtype());
+            detail::dev_sync(st.ranks[r]);
+        }
+    }
+    std::vector<void*> ptrs = replica_ptrs(rec);
+    const std::size_t bytes = s.byte_size();
+    detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        detail::check(synk_broadcast(st.handles[r], static_cast<int>(st.world), static_cast<int>(src), ptrs.data(), bytes),
+                      "broadcast");
+        detail::dev_sync(st.ranks[r]);
+    });
+    rec.coherent = true;
+}
+
+void ReplicatedVariable::all_reduce(ReduceOp op) {
+    detail::VarRecord& rec = live(rec_, "all_reduce");
+    not_gather(op, "all_reduce");
+    check_same_shapes(rec, "all_reduce");
+    detail::PoolState& st = *rec.pool;
+    std::vector<void*> ptrs = replica_ptrs(rec);
+    const std::size_t n = rec.replicas[0].size();
+    const int dt = detail::synk_dtype(rec.replicas[0].dtype());
+    detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        require_same_dtype(rec);
+        detail::check(synk_all_reduce(st.handles[r], static_cast<int>(st.world), dt, detail::synk_op(op), ptrs.data(), n),
+                      "all_reduce");
+        detail::dev_sync(st.ranks[r]);
+    });
+    rec.coherent = true;
+}
+
+void ReplicatedVariable::reduce(ReduceOp op, std::size_t dst) {
+    detail::VarRecord& rec = live(rec_, "reduce");
+    not_gather(op, "reduce");
+    check_rank(rec, dst, "reduce");
+    check_same_shapes(rec, "reduce");
+    detail::PoolState& st = *rec.pool;
+    std::vector<void*> ptrs = replica_ptrs(rec);
+    const DevBuffer& first = rec.replicas[0];
+    DevBuffer folded;
+    detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        if (r != dst) return;
+        require_same_dtype(rec);
+        folded = DevBuffer::alloc(st.ranks[r], first.shape(), first.dtype());
+        detail::check(synk_tree_reduce(st.handles[r], static_cast<int>(st.world), detail::synk_dtype(first.dtype()),
+                                       detail::synk_op(op), ptrs.data(), first.size(), folded.data()),
+                      "reduce");
+        detail::dev_sync(st.ranks[r]);
+    });
+    rec.replicas[dst] = std::move(folded);
+    if (rec.replicas.size() > 1) rec.coherent = false;
+}
+
+NdBuffer ReplicatedVariable::gather() const {
+    detail::VarRecord& rec = live(rec_, "gather");
+    detail::PoolState& st = *rec.pool;
+    // concat_rows validation (tensor.cpp:287-313) happens on rank 0 inside
+    // the phase in the reference, so its errors surface as PhaseError.
+    std::string problem;
+    std::size_t total = 0;
+    std::vector<std::size_t> offsets;
+    const DevBuffer& head = rec.replicas[0];
+    for (const DevBuffer& p : rec.replicas) {
+        if (p.rank() == 0) {
+            problem = "rows(): a rank-0 buffer has no leading dimension";
+            break;
+        }
+        if (p.dtype() != head.dtype()) {
+            problem = "concat_rows(): parts mix dtypes";
+            break;
+        }
+        if (p.rank() != head.rank() || !std::equal(p.shape().begin() + 1, p.shape().end(), head.shape().begin() + 1)) {
+            problem = "concat_rows(): trailing shapes differ";
+            break;
+        }
+        total += p.rows();
+    }
+    NdBuffer out;
+    if (problem.empty()) {
+        std::vector<std::size_t> shape = head.shape();
+        shape[0] = total;
+        out = NdBuffer::uninitialized(std::move(shape), head.dtype());
+        std::size_t row_bytes = head.row_size() * dtype_size(head.dtype()), at = 0;
+        for (std::size_t r = 0; r < rec.replicas.size(); ++r) {
+            offsets.push_back(at);
+            at += rec.replicas[r].rows() * row_bytes;
+        }
+    }
+    detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        if (!problem.empty()) {
+            if (r == 0) {
+                if (problem.rfind("concat_rows(): parts", 0) == 0) throw DTypeError(problem);
+                throw ShapeError(problem);
+            }
+            return;
+        }
+        detail::dev_to_host_into(rec.replicas[r], out.bytes_mut() + offsets[r]);
+        detail::dev_sync(st.ranks[r]);
+    });
+    return out;
+}
+
+NdBuffer ReplicatedVariable::get_value(std::size_t rank) const {
+    detail::VarRecord& rec = live(rec_, "get_value");
+    check_rank(rec, rank, "get_value");
+    no_phase(rec, "get_value");
+    return detail::dev_to_host(rec.replicas[rank]);
+}
+
+void ReplicatedVariable::set_value(std::size_t rank, const NdBuffer& value) {
+    detail::VarRecord& rec = live(rec_, "set_value");
+    check_rank(rec, rank, "set_value");
+    no_phase(rec, "set_value");
+    const auto& rd = rec.pool->ranks[rank];
+    rec.replicas[rank] = detail::dev_from_host(rd, value);
+    detail::dev_sync(rd);
+    if (rec.replicas.size() > 1) rec.coherent = false;
+}
+
+void ReplicatedVariable::scatter_value(const NdBuffer& data, const std::optional<IndexSelection>& indexes) {
+    detail::VarRecord& rec = live(rec_, "scatter_value");
+    const std::size_t n = data.rows();
+    std::size_t eff = n;
+    if (indexes) {
+        validate_selection(*indexes, n);
+        eff = selection_count(*indexes);
+    }
+    std::vector<RowRange> parts = partition_rows(eff, rec.replicas.size());
+    detail::PoolState& st = *rec.pool;
+    detail::run_pool_phase(st, PhaseKind::ScatterVar, [&](std::size_t r) {
+        // Fresh HBM storage per rank (never aliases the source, replicated.cpp:186-188).
+        rec.replicas[r] = detail::excerpt_to_device(st.ranks[r], data, nullptr, indexes, parts[r]);
+        detail::dev_sync(st.ranks[r]);
+    });
+    if (rec.replicas.size() > 1) rec.coherent = false;
+}
+
+void ReplicatedVariable::scatter_value(const SharedInputArray& data, const std::optional<IndexSelection>& indexes) {
+    scatter_value(data.view(), indexes);
+}
+
+bool ReplicatedVariable::replicas_coherent() const {
+    detail::VarRecord& rec = live(rec_, "replicas_coherent");
+    no_phase(rec, "replicas_coherent");
+    const DevBuffer& a = rec.replicas[0];
+    for (std::size_t r = 1; r < rec.replicas.size(); ++r) {
+        const DevBuffer& b = rec.replicas[r];
+        if (b.dtype() != a.dtype() || !b.same_shape(a)) return false;
+        int eq = 1;
+        detail::check(synk_equal(b.owner()->h, b.data(), a.data(), a.byte_size(), &eq), "replicas_coherent");
+        if (!eq) return false;
+    }
+    return true;
+}
+
+DevBuffer ReplicatedVariable::device_value(std::size_t rank) const {
+    detail::VarRecord& rec = live(rec_, "device_value");
+    check_rank(rec, rank, "device_value");
+    return rec.replicas[rank];
+}
+
+} // namespace synkpar

@@ -1,0 +1,286 @@
+// Optimizers, flat parameter block and the synchronous trainer (sgd.hpp).
+
+#include "synkpar/sgd.hpp"
+
+#include <chrono>
+#include <cmath>
+
+#include "internal.hpp"
+
+namespace synkpar {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+std::size_t aux_needed(const UpdateRule& r) noexcept {
+    if (std::holds_alternative<SgdRule>(r)) return 0;
+    return std::holds_alternative<AdamRule>(r) ? 2 : 1;
+}
+
+int rule_code(const UpdateRule& r) {
+    if (std::holds_alternative<SgdRule>(r)) return SYNK_RULE_SGD;
+    if (std::holds_alternative<MomentumRule>(r)) return SYNK_RULE_MOMENTUM;
+    if (std::holds_alternative<RmsPropRule>(r)) return SYNK_RULE_RMSPROP;
+    return SYNK_RULE_ADAM;
+}
+
+std::vector<double> rule_hyper(const UpdateRule& r) {
+    if (const auto* m = std::get_if<MomentumRule>(&r)) return {m->mu};
+    if (const auto* p = std::get_if<RmsPropRule>(&r)) return {p->rho, p->eps};
+    if (const auto* a = std::get_if<AdamRule>(&r)) return {a->beta1, a->beta2, a->eps};
+    return {0.0};
+}
+
+void check_step(const OptimizerState& st, const NdBuffer& p, const NdBuffer& g, const char* who) {
+    if (p.dtype() != g.dtype()) throw DTypeError(std::string(who) + ": params/grads dtype mismatch");
+    if (p.size() != g.size())
+        throw ShapeError(std::string(who) + ": params length " + std::to_string(p.size()) + " != grads length " +
+                         std::to_string(g.size()));
+    if (st.aux.size() != aux_needed(st.rule))
+        throw ArgumentError(std::string(who) + ": optimizer state holds " + std::to_string(st.aux.size()) +
+                            " auxiliary buffers, rule needs " + std::to_string(aux_needed(st.rule)));
+    for (const NdBuffer& a : st.aux)
+        if (a.size() != p.size() || a.dtype() != p.dtype())
+            throw ShapeError(std::string(who) + ": auxiliary buffer does not match params");
+}
+
+// Host-buffer step on the GPU: H2D, one update kernel, D2H back in place.
+void device_step(OptimizerState& st, NdBuffer& params, const NdBuffer& grads, const char* who) {
+    check_step(st, params, grads, who);
+    st.t += 1;
+    auto rd = detail::utility_device();
+    DevBuffer p = detail::dev_from_host(rd, params);
+    DevBuffer g = detail::dev_from_host(rd, grads);
+    std::vector<DevBuffer> aux;
+    for (const NdBuffer& a : st.aux) aux.push_back(detail::dev_from_host(rd, a));
+    std::vector<double> hyper = rule_hyper(st.rule);
+    detail::check(synk_optimizer_step(rd->h, detail::synk_dtype(params.dtype()), rule_code(st.rule), hyper.data(), st.lr,
+                                      st.t, p.data(), g.data(), aux.size() > 0 ? aux[0].data() : nullptr,
+                                      aux.size() > 1 ? aux[1].data() : nullptr, params.size()),
+                  who);
+    if (params.byte_size()) detail::dev_to_host_into(p, params.bytes_mut());
+    for (std::size_t i = 0; i < aux.size(); ++i)
+        if (st.aux[i].byte_size()) detail::dev_to_host_into(aux[i], st.aux[i].bytes_mut());
+    detail::dev_sync(rd);
+}
+
+template <class R>
+void require_rule(const OptimizerState& st, const char* who) {
+    if (!std::holds_alternative<R>(st.rule)) throw ArgumentError(std::string(who) + ": optimizer state holds another rule");
+}
+
+} // namespace
+
+const char* update_rule_name(const UpdateRule& r) noexcept {
+    if (std::holds_alternative<SgdRule>(r)) return "sgd";
+    if (std::holds_alternative<MomentumRule>(r)) return "momentum";
+    if (std::holds_alternative<RmsPropRule>(r)) return "rmsprop";
+    return "adam";
+}
+
+OptimizerState make_optimizer(UpdateRule rule, double lr, std::size_t n, DType dtype) {
+    OptimizerState st;
+    st.rule = rule;
+    st.lr = lr;
+    for (std::size_t i = 0; i < aux_needed(rule); ++i) st.aux.push_back(NdBuffer::zeros({n}, dtype));
+    return st;
+}
+
+void step_sgd(OptimizerState& st, NdBuffer& p, const NdBuffer& g) {
+    require_rule<SgdRule>(st, "step_sgd");
+    device_step(st, p, g, "step_sgd");
+}
+void step_momentum(OptimizerState& st, NdBuffer& p, const NdBuffer& g) {
+    require_rule<MomentumRule>(st, "step_momentum");
+    device_step(st, p, g, "step_momentum");
+}
+void step_rmsprop(OptimizerState& st, NdBuffer& p, const NdBuffer& g) {
+    require_rule<RmsPropRule>(st, "step_rmsprop");
+    device_step(st, p, g, "step_rmsprop");
+}
+void step_adam(OptimizerState& st, NdBuffer& p, const NdBuffer& g) {
+    require_rule<AdamRule>(st, "step_adam");
+    device_step(st, p, g, "step_adam");
+}
+void apply_update(OptimizerState& st, NdBuffer& p, const NdBuffer& g) {
+    device_step(st, p, g, update_rule_name(st.rule));
+}
+
+bool all_finite(const NdBuffer& buf) noexcept {
+    // Host-side debug predicate over a host buffer.
+    for (std::size_t i = 0; i < buf.size(); ++i)
+        if (!std::isfinite(buf.get(i))) return false;
+    return true;
+}
+
+// ---- flat block --------------------------------------------------------------------
+
+FlatParamBlock FlatParamBlock::create(WorkerPool& pool, std::span<const NdBuffer> initial) {
+    FlatPack pack = flatten_concat(initial);
+    FlatParamBlock b;
+    b.segments = std::move(pack.segments);
+    b.length = pack.flat.size();
+    b.params = replicate(pool, pack.flat);
+    b.grads = replicate(pool, NdBuffer::zeros({b.length}, pack.flat.dtype()));
+    return b;
+}
+
+std::vector<NdBuffer> FlatParamBlock::read_params(std::size_t rank) const {
+    return unflatten(params.get_value(rank), segments);
+}
+
+// ---- trainer -----------------------------------------------------------------------------
+
+SyncSgd::SyncSgd(WorkerPool& pool, FlatParamBlock block, UpdateRule rule, double lr, TrainerOptions opts)
+    : pool_(&pool), block_(std::move(block)), opts_(opts), rule_(rule), lr_(lr) {
+    const DType dt = block_.params.dtype();
+    const std::size_t naux = aux_needed(rule_);
+    for (std::size_t i = 0; i < naux; ++i) aux_.push_back(replicate(pool, NdBuffer::zeros({block_.length}, dt)));
+
+    // The per-rank step function (used when gradients are not all-reduced;
+    // with the all-reduce on, train_step fuses reduce + update instead).
+    Kernel k;
+    k.name = std::string("step_") + update_rule_name(rule_);
+    k.arity = 1;
+    k.reads = {block_.params, block_.grads};
+    for (const ReplicatedVariable& a : aux_) k.reads.push_back(a);
+    std::vector<std::uint64_t> ids{block_.params.id()};
+    for (const ReplicatedVariable& a : aux_) ids.push_back(a.id());
+    const int code = rule_code(rule_);
+    const std::vector<double> hyper = rule_hyper(rule_);
+    const double lr_copy = lr_;
+    const std::uint64_t* t_ptr = &t_;
+    k.device_fn = [ids, code, hyper, lr_copy, naux, t_ptr](const std::vector<DevBuffer>&, const KernelContext& ctx) {
+        const DevBuffer& p0 = ctx.device_replica(0);
+        const DevBuffer& g = ctx.device_replica(1);
+        if (p0.dtype() != g.dtype()) throw DTypeError("step: params/grads dtype mismatch");
+        if (p0.size() != g.size()) throw ShapeError("step: params length != grads length");
+        DevBuffer p = detail::dev_clone(ctx.rank_device, p0);
+        std::vector<DevBuffer> aux;
+        for (std::size_t i = 0; i < naux; ++i) aux.push_back(detail::dev_clone(ctx.rank_device, ctx.device_replica(2 + i)));
+        detail::check(synk_optimizer_step(ctx.dev, detail::synk_dtype(p.dtype()), code, hyper.data(), lr_copy, *t_ptr + 1,
+                                          p.data(), g.data(), naux > 0 ? aux[0].data() : nullptr,
+                                          naux > 1 ? aux[1].data() : nullptr, p.size()),
+                      "optimizer step");
+        DeviceKernelResult r;
+        r.updates.push_back({ids[0], p, UpdateCombine::Overwrite});
+        for (std::size_t i = 0; i < naux; ++i) r.updates.push_back({ids[1 + i], aux[i], UpdateCombine::Overwrite});
+        return r;
+    };
+    std::vector<UpdateSpec> specs{UpdateSpec{block_.params, UpdateCombine::Overwrite}};
+    for (const ReplicatedVariable& a : aux_) specs.push_back(UpdateSpec{a, UpdateCombine::Overwrite});
+    f_step_ = function(pool, std::move(k), {InputSpec{InputMode::Broadcast}}, {}, std::move(specs));
+    distribute(pool);
+}
+
+double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<FunctionArg>& batch,
+                           const CallOptions& call_opts) {
+    const auto t0 = Clock::now();
+    StepReport rep;
+    auto st = detail::state_of(*pool_);
+    const std::size_t W = st->world;
+
+    const auto combine = f_grad.update_combine_for(block_.grads.id());
+    if (!combine) throw ArgumentError("train_step(): gradient function does not update the gradient block");
+    auto& grads = detail::replicas_of(block_.grads);
+    if (*combine == UpdateCombine::Add) {
+        // Accumulating gradient functions start from zero every step.
+        for (std::size_t r = 0; r < W; ++r) block_.grads.set_value(r, NdBuffer::zeros({block_.length}, block_.grads.dtype()));
+    }
+
+    CallResult gr = f_grad.call(batch, call_opts);
+    if (gr.outputs.empty()) throw ArgumentError("train_step(): gradient function must output the loss");
+    const double loss = gr.outputs[0].get(0);
+    rep.grad_call = gr.report;
+
+    if (opts_.check_finite) {
+        for (std::size_t r = 0; r < W; ++r) {
+            int ok = 1;
+            detail::check(synk_all_finite(grads[r].owner()->h, detail::synk_dtype(grads[r].dtype()), grads[r].data(),
+                                          grads[r].size(), &ok),
+                          "check_finite");
+            if (!ok) throw NumericError("train_step(): non-finite gradient elements on rank " + std::to_string(r));
+        }
+    }
+
+    if (opts_.all_reduce) {
+        if (opts_.grad_op == ReduceOp::Gather) throw ArgumentError("all_reduce: Gather is not a reduction (use gather())");
+        for (std::size_t r = 1; r < W; ++r)
+            if (!grads[r].same_shape(grads[0]))
+                throw ShapeError("all_reduce: replica shapes differ across ranks (" + grads[0].shape_string() + " vs rank " +
+                                 std::to_string(r) + " " + grads[r].shape_string() + ")");
+        // Unequal shards: pre-scale each rank's shard-mean gradient by
+        // rows_r*W/total so the equal-weight mean is the global row mean.
+        std::vector<double> factor(W, 1.0);
+        bool unequal = false;
+        if (opts_.grad_op == ReduceOp::Mean) {
+            const auto& rows = gr.report.rank_rows;
+            std::size_t total = 0;
+            for (std::size_t x : rows) total += x;
+            for (std::size_t r = 0; r < rows.size(); ++r) unequal |= rows[r] * W != total;
+            if (unequal && total > 0)
+                for (std::size_t r = 0; r < W; ++r) factor[r] = double(rows[r]) * double(W) / double(total);
+            unequal = unequal && total > 0;
+        }
+        auto& params = detail::replicas_of(block_.params);
+        std::vector<void*> pp, gp, a0, a1;
+        for (std::size_t r = 0; r < W; ++r) {
+            pp.push_back(params[r].data());
+            gp.push_back(grads[r].data());
+            if (aux_.size() > 0) a0.push_back(detail::replicas_of(aux_[0])[r].data());
+            if (aux_.size() > 1) a1.push_back(detail::replicas_of(aux_[1])[r].data());
+        }
+        bool coherent = detail::record_of(block_.params).coherent;
+        for (const ReplicatedVariable& a : aux_) coherent = coherent && detail::record_of(a).coherent;
+        const std::vector<double> hyper = rule_hyper(rule_);
+        const int code = rule_code(rule_);
+        const std::uint64_t t_next = t_ + 1;
+        const auto ta = Clock::now();
+        if (unequal) {
+            // Rank-local pre-scale (sgd.cpp:292-312 semantics, T(f64 g * factor)).
+            // It must complete on every rank before any rank reads peers, hence
+            // its own phase.
+            detail::run_pool_phase(*st, PhaseKind::Collective, [&](std::size_t r) {
+                const auto& rd = st->ranks[r];
+                detail::check(synk_scale(rd->h, detail::synk_dtype(grads[r].dtype()), grads[r].data(), factor[r],
+                                         grads[r].size()),
+                              "unequal-shard pre-scale");
+                detail::dev_sync(rd);
+            });
+        }
+        PhaseReport ph2 = detail::run_pool_phase(*st, PhaseKind::Collective, [&](std::size_t r) {
+            const auto& rd = st->ranks[r];
+            if (params[r].dtype() != grads[r].dtype()) throw DTypeError("step: params/grads dtype mismatch");
+            if (params[r].size() != grads[r].size()) throw ShapeError("step: params length != grads length");
+            detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), detail::synk_dtype(grads[r].dtype()),
+                                               detail::synk_op(opts_.grad_op), code, hyper.data(), lr_, t_next, pp.data(),
+                                               gp.data(), a0.empty() ? nullptr : a0.data(),
+                                               a1.empty() ? nullptr : a1.data(), grads[r].size(), coherent ? 1 : 0),
+                          "fused all-reduce + update");
+            detail::dev_sync(rd);
+        });
+        rep.allreduce_s = since(ta);
+        rep.step_call.rank_compute_s = ph2.rank_seconds;
+        rep.step_call.rank_rows.assign(W, 1);
+        rep.step_call.straggler_s = ph2.straggler_seconds();
+        rep.step_call.total_s = ph2.max_seconds();
+        detail::record_of(block_.grads).coherent = true;
+        detail::record_of(block_.params).coherent = true;
+        for (const ReplicatedVariable& a : aux_) detail::record_of(a).coherent = true;
+    } else {
+        CallResult sr = f_step_.call({FunctionArg(NdBuffer::scalar(double(t_ + 1)))});
+        rep.step_call = sr.report;
+    }
+    t_ += 1;
+
+    if (opts_.verify_coherence && !block_.params.replicas_coherent())
+        throw CoherenceError("train_step(): parameter replicas diverged after step " + std::to_string(t_));
+    rep.loss = loss;
+    rep.total_s = since(t0);
+    last_ = rep;
+    return loss;
+}
+
+} // namespace synkpar
