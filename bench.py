@@ -80,7 +80,7 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "100"],
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -256,7 +256,13 @@ def ours(args, n_gpus):
         return max(region), float(np.mean(launch))
 
     with ClockSampler(n_gpus) as clocks:
+        # Soak under the same load first so nvidia-smi (200 ms cadence) samples
+        # clocks around the timed region even when K steps take milliseconds.
+        t_soak = time.time()
+        while time.time() - t_soak < 1.5:
+            gather_launches(n_step, 16, 0)
         region_s, launch_s = gather_launches(n_step, args.steps, args.warmup)
+        time.sleep(0.25)
     bytes_step = n_gpus * n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA)
     value = bytes_step * args.steps / region_s / 1e9
     achieved = n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA) / launch_s / 1e9

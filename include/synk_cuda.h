@@ -182,6 +182,29 @@ int synk_all_reduce_step(synk_dev* dev, int world, int dtype, int grad_op, int r
                          void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
                          int replicas_coherent);
 
+/* ---- tensor-core GEMM (the MLP's dense products, mlp.cpp:31-73) -------------------- */
+#define SYNK_BF16 3     /* storage code for bf16 operands/outputs (new; DType has f32/f64) */
+#define SYNK_GEMM_BF16 0   /* tcgen05 kind::f16, bf16 operands, fp32 accumulate          */
+#define SYNK_GEMM_TF32 1   /* tcgen05 kind::tf32, one pass                                 */
+#define SYNK_GEMM_TF32X3 2 /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi (fp32 accuracy)    */
+#define SYNK_EPI_STORE 0
+#define SYNK_EPI_BIAS 1      /* + bias[n]                                                 */
+#define SYNK_EPI_BIAS_TANH 2 /* tanh(. + bias[n])                       (mlp.cpp:169-176) */
+#define SYNK_EPI_TANH_GRAD 3 /* . * (1 - act[m,n]^2)                    (mlp.cpp:206-208) */
+/* Operand staging for synk_gemm_tc: out = in (or in^T when transpose) as
+ * mode 0: tf32 hi/lo split (out_hi, out_lo fp32), 1: bf16 cast, 2: fp32 copy;
+ * out is out_rows x out_cols with leading dim ld_out, zero beyond the input. */
+int synk_gemm_prep(synk_dev* dev, int in_dtype, const void* in, uint64_t rows, uint64_t cols, uint64_t ld_in,
+                   int transpose, int mode, void* out_hi, float* out_lo, uint64_t out_rows, uint64_t out_cols,
+                   uint64_t ld_out);
+/* C[M x N] = epilogue(A[M x K] . B[N x K]^T); A, B K-major with leading dims
+ * lda/ldb (16-byte aligned rows). C (row-major, ldc) and/or C^T (ldct) may be
+ * NULL; out_dtype SYNK_F32 or SYNK_BF16 (act has the same dtype as C). */
+int synk_gemm_tc(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
+                 uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int epilogue, int out_dtype,
+                 void* c, uint64_t ldc, void* ct, uint64_t ldct, const float* bias, const void* act,
+                 uint64_t ldact);
+
 /* ---- example function: tanh MLP loss + gradient (mlp.cpp:134-218) ---------------- */
 /* dims[0..layers]; params flat [W0 b0 W1 b1 ...]; x [n x dims0]; y [n x dims_L].
  * Writes the f64 loss scalar to loss_dev (device) and the flat gradient (dtype)

@@ -1,0 +1,407 @@
+// Tensor-core GEMM for the example function's dense products, sm_100a only:
+//   C[M x N] = epilogue( A[M x K] . B[N x K]^T )     (A, B K-major in HBM)
+//
+// One 128 x 128 output tile per CTA (4 warps):
+//   warp 0 / one lane : TMA producer — cp.async.bulk.tensor 2-D loads of
+//                       128 x 128-byte A and B boxes (SWIZZLE_128B) into a
+//                       kStages-deep shared-memory ring, mbarrier complete_tx
+//   warp 1 / one lane : MMA issuer — tcgen05.mma.cta_group::1 (kind::f16 for
+//                       bf16 operands, kind::tf32 for fp32 operands) with the
+//                       fp32 accumulator in TMEM (128 lanes x 128 columns);
+//                       tcgen05.commit releases each smem stage and finally
+//                       signals the epilogue
+//   warp 2            : TMEM allocation / deallocation
+//   all 4 warps       : epilogue — tcgen05.ld 32x32b (thread t owns tile row
+//                       t), fused bias / tanh / tanh-derivative, stores to C
+//                       (and optionally to C^T, which this lane layout makes
+//                       fully coalesced).
+//
+// fp32 accuracy on tensor cores ("3xTF32"): operands are pre-split into
+// tf32 hi + lo parts (synk_split_tf32) and the kernel accumulates
+// hi*hi + hi*lo + lo*hi in the same TMEM accumulator (3 passes over K), which
+// keeps the error at fp32 level (the north_star's 1e-5 fp32 bar) while every
+// multiply runs on the tensor pipe.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 128, BN = 128, kThreads = 128, kStages = 4;
+constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 bytes, one operand, one stage
+
+enum Epi { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_TANH = 2, EPI_TANH_GRAD = 3 };
+
+// ---- PTX wrappers ---------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// K-major, 128-byte swizzled operand tile: 8-row core groups 1024 bytes apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)(16 >> 4) << 16;    // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: next 8-row group
+    d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+template <int KIND>  // 0 = kind::f16 (bf16), 1 = kind::tf32
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    if constexpr (KIND == 0) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    }
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Instruction descriptor: fp32 accumulate, K-major A and B, M = 128, N = 128.
+template <int KIND>
+__host__ __device__ constexpr uint32_t instr_desc() {
+    return (1u << 4)                        // D format f32
+           | ((KIND == 0 ? 1u : 2u) << 7)   // A format: bf16 | tf32
+           | ((KIND == 0 ? 1u : 2u) << 10)  // B format
+           | ((uint32_t)(BN >> 3) << 17)    // N
+           | ((uint32_t)(BM >> 4) << 24);   // M
+}
+
+struct EpiArgs {
+    int mode;
+    int out_bf16;         // store C (and C^T) as bf16 instead of fp32
+    void* c;
+    uint64_t ldc;
+    void* ct;             // optional transposed output, may be null
+    uint64_t ldct;
+    const float* bias;    // per column
+    const void* act;      // tanh activations for EPI_TANH_GRAD, same layout/dtype as C
+    uint64_t ldact;
+};
+
+__device__ __forceinline__ float load_act(const EpiArgs& e, uint64_t m, uint64_t n) {
+    if (e.out_bf16) return __bfloat162float(static_cast<const __nv_bfloat16*>(e.act)[m * e.ldact + n]);
+    return static_cast<const float*>(e.act)[m * e.ldact + n];
+}
+
+__device__ __forceinline__ void store_out(void* base, uint64_t off, float v, int bf16) {
+    if (bf16) static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(v);
+    else static_cast<float*>(base)[off] = v;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
+                   const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
+                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B atoms
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + kStages * kTileBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * kTileBytes);  // full[S], empty[S], tmem_full
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    constexpr int kBK = 128 / (KIND == 0 ? 2 : 4);  // elements per 128-byte K block
+    const int num_kb = (int)((K + kBK - 1) / kBK);
+    const int total = passes * num_kb;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&bars[s]), 1);
+            mbar_init(smem_u32(&bars[kStages + s]), 1);
+        }
+        mbar_init(smem_u32(&bars[2 * kStages]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_map(&a0);
+        prefetch_map(&b0);
+        if (passes > 1) {
+            prefetch_map(&a1);
+            prefetch_map(&b1);
+        }
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        for (int it = 0; it < total; ++it) {
+            const int s = it % kStages;
+            const uint32_t parity = ((it / kStages) & 1) ^ 1;
+            mbar_wait(smem_u32(&bars[kStages + s]), parity);
+            const int pass = it / num_kb, kb = it % num_kb;
+            const CUtensorMap* ma = pass == 2 ? &a1 : &a0;  // passes: hi.hi, hi.lo, lo.hi
+            const CUtensorMap* mb = pass == 1 ? &b1 : &b0;
+            const uint32_t full = smem_u32(&bars[s]);
+            mbar_expect_tx(full, 2 * kTileBytes);
+            tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, kb * kBK, (int)m0);
+            tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, kb * kBK, (int)n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idesc = instr_desc<KIND>();
+        for (int it = 0; it < total; ++it) {
+            const int s = it % kStages;
+            mbar_wait(smem_u32(&bars[s]), (it / kStages) & 1);
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(sa + s * kTileBytes), b_base = smem_u32(sb + s * kTileBytes);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K slices per 128-byte row (UMMA_K = 16 bf16 | 8 tf32)
+                umma<KIND>(tmem, smem_desc(a_base + 32 * k), smem_desc(b_base + 32 * k), idesc,
+                           (it > 0 || k > 0) ? 1u : 0u);
+            }
+            umma_commit(smem_u32(&bars[kStages + s]));  // smem stage free once these MMAs retire
+        }
+        umma_commit(smem_u32(&bars[2 * kStages]));     // accumulator complete
+    }
+    __syncwarp();
+
+    // ---- epilogue: TMEM -> registers -> fused elementwise -> HBM ----
+    mbar_wait(smem_u32(&bars[2 * kStages]), 0);
+    tc_fence_after();
+    const uint64_t m = m0 + warp * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(lane_base + c0, r);
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t n = n0 + c0 + j;
+            if (n >= N) break;
+            float v = __uint_as_float(r[j]);
+            if (epi.mode == EPI_BIAS) v += epi.bias[n];
+            else if (epi.mode == EPI_BIAS_TANH) v = tanhf(v + epi.bias[n]);
+            else if (epi.mode == EPI_TANH_GRAD) {
+                const float a = load_act(epi, m, n);
+                v = v * (1.0f - a * a);
+            }
+            if (epi.c) store_out(epi.c, m * epi.ldc + n, v, epi.out_bf16);
+            if (epi.ct) store_out(epi.ct, n * epi.ldct + m, v, epi.out_bf16);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    }
+}
+
+// ---- host side: tensor maps ---------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// rows x k matrix, K-major with leading dimension ld (elements); box = 128 rows x 128 bytes.
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t ld, bool bf16) {
+    EncodeFn enc = encoder();
+    SYNK_REQUIRE(enc != nullptr, SYNK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const uint64_t es = bf16 ? 2 : 4;
+    SYNK_REQUIRE(((uintptr_t)base % 16) == 0 && (ld * es) % 16 == 0, SYNK_EARG,
+                 "gemm_tc: operand base and row pitch must be 16-byte aligned");
+    cuuint64_t dims[2] = {k, rows};
+    cuuint64_t strides[1] = {ld * es};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / es), 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SYNK_REQUIRE(r == CUDA_SUCCESS, SYNK_ECUDA, "cuTensorMapEncodeTiled failed");
+    return SYNK_OK;
+}
+
+constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+template <int KIND>
+int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+           const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e) {
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[KIND]) {
+        SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+        attr_set[KIND] = true;
+    }
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    gemm_tc_kernel<KIND><<<grid, kThreads, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
+                                                                   (uint32_t)K, e);
+    SYNK_LAUNCHED("gemm_tc_kernel");
+    return SYNK_OK;
+}
+
+// ---- operand preparation: tf32 hi/lo split, bf16 cast, optional transpose -------------
+
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// out[r][c] (ld_out, zero-padded to cols_pad) from in (rows x cols, ld_in), or
+// the transpose (out[c][r], cols x rows, zero-padded to rows_pad) when trans.
+// Tiled 32x32 through shared memory so both sides stay coalesced.
+template <class In>
+__global__ void __launch_bounds__(256) prep_kernel(const In* __restrict__ in, uint64_t rows, uint64_t cols,
+                                                   uint64_t ld_in, int trans, int mode, void* __restrict__ out_hi,
+                                                   float* __restrict__ out_lo, uint64_t out_rows, uint64_t out_cols,
+                                                   uint64_t ld_out) {
+    __shared__ float tile[32][33];
+    const uint64_t r0 = (uint64_t)blockIdx.y * 32, c0 = (uint64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+    // load in-tile (input coordinates) covering the output tile
+    for (int k = ty; k < 32; k += 8) {
+        uint64_t ir, ic;
+        if (!trans) { ir = r0 + k; ic = c0 + tx; }
+        else { ir = c0 + k; ic = r0 + tx; }  // output (r,c) = input (c,r): tile over output coords
+        float v = 0.f;
+        if (ir < rows && ic < cols) v = (float)in[ir * ld_in + ic];
+        tile[k][tx] = v;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const uint64_t orow = r0 + k, ocol = c0 + tx;
+        if (orow >= out_rows || ocol >= out_cols) continue;
+        const float v = trans ? tile[tx][k] : tile[k][tx];
+        const uint64_t o = orow * ld_out + ocol;
+        if (mode == 0) {  // tf32 split
+            const float hi = to_tf32(v);
+            static_cast<float*>(out_hi)[o] = hi;
+            out_lo[o] = to_tf32(v - hi);
+        } else if (mode == 1) {  // bf16 cast
+            static_cast<__nv_bfloat16*>(out_hi)[o] = __float2bfloat16_rn(v);
+        } else {  // plain fp32 copy (single-pass tf32)
+            static_cast<float*>(out_hi)[o] = v;
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int synk_gemm_prep(synk_dev* d, int in_dtype, const void* in, uint64_t rows, uint64_t cols, uint64_t ld_in,
+                   int transpose, int mode, void* out_hi, float* out_lo, uint64_t out_rows, uint64_t out_cols,
+                   uint64_t ld_out) {
+    SYNK_REQUIRE(in_dtype == SYNK_F32 || in_dtype == 3, SYNK_EDTYPE, "gemm_prep: input must be f32 or bf16");
+    if (out_rows == 0 || out_cols == 0) return SYNK_OK;
+    synk::DeviceGuard g(d->device);
+    dim3 grid((unsigned)((out_cols + 31) / 32), (unsigned)((out_rows + 31) / 32));
+    if (in_dtype == SYNK_F32)
+        prep_kernel<float><<<grid, 256, 0, d->stream>>>((const float*)in, rows, cols, ld_in, transpose, mode, out_hi,
+                                                        out_lo, out_rows, out_cols, ld_out);
+    else
+        prep_kernel<__nv_bfloat16><<<grid, 256, 0, d->stream>>>((const __nv_bfloat16*)in, rows, cols, ld_in, transpose,
+                                                                mode, out_hi, out_lo, out_rows, out_cols, ld_out);
+    SYNK_LAUNCHED("prep_kernel");
+    return SYNK_OK;
+}
+
+int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
+                 uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int epilogue, int out_dtype, void* c,
+                 uint64_t ldc, void* ct, uint64_t ldct, const float* bias, const void* act, uint64_t ldact) {
+    SYNK_REQUIRE(kind >= 0 && kind <= 2, SYNK_EARG, "gemm_tc: kind is 0 (bf16), 1 (tf32) or 2 (3xtf32)");
+    SYNK_REQUIRE(out_dtype == SYNK_F32 || out_dtype == 3, SYNK_EDTYPE, "gemm_tc: output f32 or bf16");
+    SYNK_REQUIRE(M < (1ull << 31) && N < (1ull << 31) && K < (1ull << 31), SYNK_EARG, "gemm_tc: dims too large");
+    if (M == 0 || N == 0) return SYNK_OK;
+    synk::DeviceGuard g(d->device);
+    const bool bf16 = kind == 0;
+    CUtensorMap a0, a1, b0, b1;
+    if (int rc = make_map(&a0, a_hi, M, K, lda, bf16); rc) return rc;
+    if (int rc = make_map(&b0, b_hi, N, K, ldb, bf16); rc) return rc;
+    a1 = a0;
+    b1 = b0;
+    if (kind == 2) {
+        SYNK_REQUIRE(a_lo && b_lo, SYNK_EARG, "gemm_tc: 3xtf32 needs lo parts");
+        if (int rc = make_map(&a1, a_lo, M, K, lda, false); rc) return rc;
+        if (int rc = make_map(&b1, b_lo, N, K, ldb, false); rc) return rc;
+    }
+    EpiArgs e{epilogue, out_dtype == 3, c, ldc, ct, ldct, bias, act, ldact};
+    if (K == 0) return synk::fail(SYNK_EARG, "gemm_tc: K must be > 0");
+    return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e)
+                : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, e);
+}
+
+}  // extern "C"

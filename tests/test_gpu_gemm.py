@@ -1,0 +1,107 @@
+"""tcgen05 tensor-core GEMM (synk_gemm_tc) parity against an fp64 reference.
+
+Tolerances: 3xTF32 keeps fp32-level error (elem_err <= 1e-5 relative to the
+problem scale at K <= 4096); single-pass TF32 and BF16 are checked at their
+own mantissa widths (2^-10 / 2^-7 relative, times sqrt(K) growth headroom).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from cabi import F32, Ranks, check, lib
+
+pytestmark = pytest.mark.gpu
+_u64 = ctypes.c_uint64
+_vp = ctypes.c_void_p
+BF16 = 3
+KIND = {"bf16": 0, "tf32": 1, "tf32x3": 2}
+EPI = {"store": 0, "bias": 1, "bias_tanh": 2, "tanh_grad": 3}
+
+
+def pad(n, m):
+    return (n + m - 1) // m * m
+
+
+def prep(R, x, transpose, mode):
+    """Stage a host fp32 matrix for the GEMM (K-major, 16-byte rows)."""
+    rows, cols = x.shape
+    orows, ocols = (cols, rows) if transpose else (rows, cols)
+    ld = pad(ocols, 8)
+    dx = R.upload(np.ascontiguousarray(x, np.float32))
+    es = 2 if mode == 1 else 4
+    hi = R.alloc(orows * ld * es)
+    lo = R.alloc(orows * ld * 4) if mode == 0 else 0
+    check(lib().synk_gemm_prep(R[0], F32, _vp(dx), _u64(rows), _u64(cols), _u64(cols), int(transpose), mode,
+                               _vp(hi), _vp(lo or None), _u64(orows), _u64(ocols), _u64(ld)), "prep")
+    return hi, lo, ld
+
+
+def gemm(R, kind, a, b, epi="store", bias=None, act=None, want_t=False):
+    """C = epi(a @ b.T) with a: [M,K], b: [N,K] (host fp32)."""
+    M, K = a.shape
+    N = b.shape[0]
+    mode = {"bf16": 1, "tf32": 2, "tf32x3": 0}[kind]
+    ahi, alo, lda = prep(R, a, False, mode)
+    bhi, blo, ldb = prep(R, b, False, mode)
+    c = R.alloc(M * N * 4)
+    ct = R.alloc(M * N * 4) if want_t else 0
+    dbias = R.upload(bias.astype(np.float32)) if bias is not None else 0
+    dact = R.upload(act.astype(np.float32)) if act is not None else 0
+    check(lib().synk_gemm_tc(R[0], KIND[kind], _u64(M), _u64(N), _u64(K), _vp(ahi), _vp(alo or None), _u64(lda),
+                             _vp(bhi), _vp(blo or None), _u64(ldb), EPI[epi], F32, _vp(c), _u64(N), _vp(ct or None),
+                             _u64(M), _vp(dbias or None), _vp(dact or None), _u64(N)), "gemm")
+    check(R.sync(), "sync")
+    out = R.download(c, (M, N), np.float32)
+    out_t = R.download(ct, (N, M), np.float32) if want_t else None
+    return out, out_t
+
+
+def rel_err(got, want):
+    scale = np.maximum(1.0, np.abs(want))
+    return float(np.max(np.abs(got.astype(np.float64) - want) / scale))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 784), (200, 10, 512), (784, 512, 256), (1, 1, 8),
+                                   (300, 130, 1000)])
+def test_tf32x3_matches_fp64(M, N, K):
+    rng = np.random.default_rng(M * 7 + N + K)
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        got, got_t = gemm(R, "tf32x3", a, b, want_t=True)
+    # fp32-level: |err| <= ~K * 2^-24 * max|a||b| bound; use 1e-5 of the scale like the MLP bar
+    assert rel_err(got, want) <= 1e-5 * max(1.0, np.sqrt(K) / 8)
+    np.testing.assert_array_equal(got_t, got.T)
+
+
+@pytest.mark.parametrize("kind,tol", [("tf32", 2.0 ** -10), ("bf16", 2.0 ** -7)])
+def test_single_pass_kinds(kind, tol):
+    rng = np.random.default_rng(1)
+    M, N, K = 256, 384, 1024
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (N, K)).astype(np.float32)
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        got, _ = gemm(R, kind, a, b)
+    assert rel_err(got, want) <= tol * np.sqrt(K)
+    assert rel_err(got, want) > 0  # it really ran at reduced precision
+
+
+def test_fused_epilogues():
+    rng = np.random.default_rng(2)
+    M, N, K = 192, 160, 256
+    a = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    b = rng.uniform(-1, 1, (N, K)).astype(np.float32) * 0.1
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    act = np.tanh(rng.uniform(-1, 1, (M, N))).astype(np.float32)
+    z = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        got, _ = gemm(R, "tf32x3", a, b, "bias", bias)
+        assert rel_err(got, z + bias) <= 1e-5
+        got, _ = gemm(R, "tf32x3", a, b, "bias_tanh", bias)
+        assert rel_err(got, np.tanh(z + bias)) <= 1e-5
+        got, _ = gemm(R, "tf32x3", a, b, "tanh_grad", act=act)
+        assert rel_err(got, z * (1 - act.astype(np.float64) ** 2)) <= 1e-5

@@ -96,7 +96,16 @@ def test_combine_bit_exact(oracle, dtype, op):
             da, db = R.upload(a), R.upload(b)
             check(lib().synk_combine(R[0], cabi.dt(dtype), OPS[op], _vp(da), _vp(db), _u64(n)), "combine")
             got = R.download(da, (n,), dtype)
-            assert got.tobytes() == oracle.combine(a, b, op).tobytes()
+            want = oracle.combine(a, b, op)
+            if op in ("max", "min"):  # selects: every bit, NaN and signed zeros included
+                assert got.tobytes() == want.tobytes()
+            else:
+                # arithmetic: bit-exact on every non-NaN result; a NaN result
+                # stays NaN (x86 keeps the operand's payload, sm_100 returns
+                # the canonical NaN -- payload bits carry no value)
+                nan = np.isnan(want)
+                assert np.array_equal(np.isnan(got), nan)
+                assert got[~nan].tobytes() == want[~nan].tobytes()
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
@@ -149,8 +158,11 @@ def test_column_stats(oracle, dtype):
             # sequentially in T. Tolerance: elem_err <= rows * eps(T) (the
             # reference's own recursive-summation bound, Higham 4.2).
             tol = rows * float(np.finfo(dtype).eps)
-            exact = x.astype(np.float64).sum(axis=0)
-            assert oracle.elem_err(s, exact) <= 2 * float(np.finfo(dtype).eps)  # ours: ~1 rounding
+            exact = np.array([float(np.sum(x[:, c].astype(np.longdouble))) for c in range(cols)])
+            if dtype == np.float32:  # f64 accumulation of f32 data: one final rounding
+                assert oracle.elem_err(s, exact) <= 2 * float(np.finfo(np.float32).eps)
+            else:
+                assert oracle.elem_err(s, exact) <= tol
             assert oracle.elem_err(s, oracle.column_fold(x, "sum")) <= tol
 
 
