@@ -214,6 +214,17 @@ int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, u
 int synk_mlp_loss_grad(synk_dev* dev, int dtype, const uint64_t* dims, uint32_t layers,
                        const void* params, const void* x, const void* y, uint64_t n,
                        double* loss_dev, void* grad, void* workspace, uint64_t workspace_bytes);
+/* Same with a compute mode: SYNK_MLP_NATIVE runs every product in the
+ * parameter dtype on the CUDA cores (f32 FFMA / f64 DFMA); SYNK_MLP_BF16_TC
+ * (f32 parameters only) runs every dense product on tcgen05 tensor cores
+ * with bf16 operands and fp32 accumulation (the wide-MLP config). */
+#define SYNK_MLP_NATIVE 0
+#define SYNK_MLP_BF16_TC 1
+int synk_mlp_workspace_bytes_ex(int dtype, int compute, const uint64_t* dims, uint32_t layers, uint64_t n,
+                                uint64_t* bytes);
+int synk_mlp_loss_grad_ex(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                          const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
+                          void* grad, void* workspace, uint64_t workspace_bytes);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,10 @@
 // This file holds the SIMT path (FFMA for f32, DFMA for f64 — the f64 path
 // is what the reference's f64 trajectories are checked against at 1e-10).
 
+#include <cuda_bf16.h>
 #include <math.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -248,9 +251,183 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     return SYNK_OK;
 }
 
+// ---- bf16 tensor-core path (config C5: wide MLP, fp32 master weights) -----------------
+// Every dense product is one synk_gemm_tc (tcgen05 kind::f16) launch with all
+// operands K-major: the forward epilogue writes each hidden activation both
+// row-major (next layer's A) and transposed (its weight gradient's A), the dX
+// epilogue does the same for delta, so no separate transpose kernel touches
+// activations. Weights are cast/transposed to bf16 once per step.
+
+inline uint64_t pad8(uint64_t v) { return (v + 7) / 8 * 8; }
+
+// out[r] = sum_j in[r * ld + j], j < n (bf16 in, f32 out, f64 accumulation).
+__global__ void __launch_bounds__(256) rowsum_bf16_kernel(const __nv_bfloat16* __restrict__ in, uint64_t ld, uint64_t n,
+                                                           float* __restrict__ out) {
+    __shared__ double red[256];
+    const __nv_bfloat16* row = in + (uint64_t)blockIdx.x * ld;
+    double s = 0.0;
+    for (uint64_t j = threadIdx.x; j < n; j += 256) s += (double)__bfloat162float(row[j]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = (float)red[0];
+}
+
+struct Bf16Plan {
+    uint64_t n, maxd, L;
+    uint64_t off_w[64], off_wt[64], off_act[65], off_actT[65];
+    uint64_t off_pred, off_delta_f, off_d[2], off_dT[2], off_partial, total;
+};
+
+Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t maxd) {
+    Bf16Plan p{};
+    p.n = n;
+    p.maxd = maxd;
+    p.L = L;
+    uint64_t at = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t o = at;
+        at += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    for (uint32_t l = 0; l < L; ++l) {
+        p.off_w[l] = take(dims[l] * pad8(dims[l + 1]) * 2);
+        p.off_wt[l] = take(dims[l + 1] * pad8(dims[l]) * 2);
+    }
+    for (uint32_t l = 0; l < L; ++l) {  // act[0] = x, act[l] hidden
+        p.off_act[l] = take(n * pad8(dims[l]) * 2);
+        p.off_actT[l] = take(dims[l] * pad8(n) * 2);
+    }
+    p.off_pred = take(n * dims[L] * 4);
+    p.off_delta_f = take(n * dims[L] * 4);
+    for (int i = 0; i < 2; ++i) {
+        p.off_d[i] = take(n * pad8(maxd) * 2);
+        p.off_dT[i] = take(maxd * pad8(n) * 2);
+    }
+    p.off_partial = take(kLossBlocks * sizeof(double));
+    p.total = at;
+    return p;
+}
+
+int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P, const float* theta, const float* x,
+                   const float* y, uint64_t n, double* loss, float* grad, void* ws) {
+    Bf16Plan B = make_bf16_plan(dims, L, n, P.maxd);
+    char* base = static_cast<char*>(ws);
+    auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
+    const int F32 = SYNK_F32, BF = SYNK_BF16;
+
+    // weights: W_l (K-major for dX) and W_l^T (K-major for the forward)
+    for (uint32_t l = 0; l < L; ++l) {
+        const float* W = theta + P.woff[l];
+        if (int rc = synk_gemm_prep(d, F32, W, dims[l], dims[l + 1], dims[l + 1], 0, 1, bf(B.off_w[l]), nullptr,
+                                    dims[l], dims[l + 1], pad8(dims[l + 1]));
+            rc)
+            return rc;
+        if (int rc = synk_gemm_prep(d, F32, W, dims[l], dims[l + 1], dims[l + 1], 1, 1, bf(B.off_wt[l]), nullptr,
+                                    dims[l + 1], dims[l], pad8(dims[l]));
+            rc)
+            return rc;
+    }
+    // input batch: x and x^T in bf16
+    if (int rc = synk_gemm_prep(d, F32, x, n, dims[0], dims[0], 0, 1, bf(B.off_act[0]), nullptr, n, dims[0],
+                                pad8(dims[0]));
+        rc)
+        return rc;
+    if (int rc = synk_gemm_prep(d, F32, x, n, dims[0], dims[0], 1, 1, bf(B.off_actT[0]), nullptr, dims[0], n, pad8(n));
+        rc)
+        return rc;
+
+    // forward
+    float* pred = reinterpret_cast<float*>(base + B.off_pred);
+    for (uint32_t l = 0; l < L; ++l) {
+        const bool hidden = l + 1 < L;
+        int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, n, dims[l + 1], dims[l], bf(B.off_act[l]), nullptr, pad8(dims[l]),
+                              bf(B.off_wt[l]), nullptr, pad8(dims[l]), hidden ? SYNK_EPI_BIAS_TANH : SYNK_EPI_BIAS,
+                              hidden ? BF : F32, hidden ? (void*)bf(B.off_act[l + 1]) : (void*)pred,
+                              hidden ? pad8(dims[l + 1]) : dims[L], hidden ? (void*)bf(B.off_actT[l + 1]) : nullptr,
+                              pad8(n), theta + P.boff[l], nullptr, 0);
+        if (rc) return rc;
+    }
+
+    // loss + output delta (f32), then its bf16 operand forms
+    const uint64_t dl = dims[L], n_el = n * dl;
+    float* delta_f = reinterpret_cast<float*>(base + B.off_delta_f);
+    double* partial = reinterpret_cast<double*>(base + B.off_partial);
+    int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
+    const double inv_n = 1.0 / (double)n;
+    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial);
+    SYNK_LAUNCHED("loss_delta_kernel");
+    loss_final_kernel<<<1, 32, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
+    SYNK_LAUNCHED("loss_final_kernel");
+    int cur = 0;
+    if (int rc = synk_gemm_prep(d, F32, delta_f, n, dl, dl, 0, 1, bf(B.off_d[cur]), nullptr, n, dl, pad8(P.maxd)); rc)
+        return rc;
+    if (int rc = synk_gemm_prep(d, F32, delta_f, n, dl, dl, 1, 1, bf(B.off_dT[cur]), nullptr, dl, n, pad8(n)); rc)
+        return rc;
+    bias_grad_kernel<float><<<(unsigned)((dl + 31) / 32), kThreads, 0, d->stream>>>(delta_f, n, dl, grad + P.boff[L - 1]);
+    SYNK_LAUNCHED("bias_grad_kernel");
+
+    // backward
+    for (uint32_t l = L; l-- > 0;) {
+        const uint64_t din = dims[l], dout = dims[l + 1];
+        // gW_l = a_l^T . delta  (M = din, N = dout, K = n)
+        if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, din, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), bf(B.off_dT[cur]),
+                                  nullptr, pad8(n), SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr,
+                                  nullptr, 0);
+            rc)
+            return rc;
+        if (l + 1 < L) {  // hidden-layer bias grads from delta^T rows
+            rowsum_bf16_kernel<<<(unsigned)dout, 256, 0, d->stream>>>(bf(B.off_dT[cur]), pad8(n), n, grad + P.boff[l]);
+            SYNK_LAUNCHED("rowsum_bf16_kernel");
+        }
+        if (l > 0) {
+            // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
+            const int nxt = cur ^ 1;
+            if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, n, din, dout, bf(B.off_d[cur]), nullptr, pad8(P.maxd),
+                                      bf(B.off_w[l]), nullptr, pad8(dout), SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
+                                      pad8(P.maxd), bf(B.off_dT[nxt]), pad8(n), nullptr, bf(B.off_act[l]), pad8(din));
+                rc)
+                return rc;
+            cur = nxt;
+        }
+    }
+    return SYNK_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int synk_mlp_workspace_bytes_ex(int dtype, int compute, const uint64_t* dims, uint32_t layers, uint64_t n,
+                                uint64_t* bytes) {
+    SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "mlp: bad dtype");
+    SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || (compute == SYNK_MLP_BF16_TC && dtype == SYNK_F32), SYNK_EARG,
+                 "mlp: bf16 tensor-core compute needs f32 parameters");
+    Plan p;
+    if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
+    *bytes = compute == SYNK_MLP_NATIVE ? ws_bytes(dtype, p, n) : make_bf16_plan(dims, layers, n, p.maxd).total;
+    return SYNK_OK;
+}
+
+int synk_mlp_loss_grad_ex(synk_dev* d, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                          const void* params, const void* x, const void* y, uint64_t n, double* loss_dev, void* grad,
+                          void* workspace, uint64_t workspace_bytes) {
+    if (compute == SYNK_MLP_NATIVE)
+        return synk_mlp_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes);
+    SYNK_REQUIRE(compute == SYNK_MLP_BF16_TC && dtype == SYNK_F32, SYNK_EARG,
+                 "mlp: bf16 tensor-core compute needs f32 parameters");
+    SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
+    Plan p;
+    if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
+    SYNK_REQUIRE(workspace_bytes >= make_bf16_plan(dims, layers, n, p.maxd).total, SYNK_EARG,
+                 "mlp: workspace too small");
+    synk::DeviceGuard g(d->device);
+    return loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n, loss_dev,
+                          (float*)grad, workspace);
+}
 
 int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, uint64_t n,
                              uint64_t* bytes) {

@@ -73,17 +73,23 @@ DevBuffer as_dtype(const std::shared_ptr<detail::RankDevice>& rd, const DevBuffe
 
 // Enqueue loss + gradient on rd's stream. Returns (loss f64 scalar, grad).
 std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::RankDevice>& rd, const Checked& c,
-                                                 const DevBuffer& params, const DevBuffer& x, const DevBuffer& y) {
+                                                 const DevBuffer& params, const DevBuffer& x, const DevBuffer& y,
+                                                 MlpCompute compute = MlpCompute::Native) {
     const DType dt = params.dtype();
+    if (compute == MlpCompute::Bf16TensorCore && dt != DType::Float32)
+        throw DTypeError("mlp_grad_kernel: bf16 tensor-core compute needs float32 parameters");
+    const int mode = compute == MlpCompute::Native ? SYNK_MLP_NATIVE : SYNK_MLP_BF16_TC;
     DevBuffer xd = as_dtype(rd, x, dt), yd = as_dtype(rd, y, dt);
     const std::uint32_t L = static_cast<std::uint32_t>(c.dims.size() - 1);
     std::uint64_t ws_bytes = 0;
-    detail::check(synk_mlp_workspace_bytes(detail::synk_dtype(dt), c.dims.data(), L, c.n, &ws_bytes), "mlp workspace");
+    detail::check(synk_mlp_workspace_bytes_ex(detail::synk_dtype(dt), mode, c.dims.data(), L, c.n, &ws_bytes),
+                  "mlp workspace");
     DevBuffer ws = DevBuffer::alloc(rd, {(ws_bytes + 7) / 8}, DType::Float64);
     DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
     DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
-    detail::check(synk_mlp_loss_grad(rd->h, detail::synk_dtype(dt), c.dims.data(), L, params.data(), xd.data(), yd.data(),
-                                     c.n, static_cast<double*>(loss.data()), grad.data(), ws.data(), ws_bytes),
+    detail::check(synk_mlp_loss_grad_ex(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
+                                        yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws.data(),
+                                        ws_bytes),
                   "mlp_loss_grad");
     return {loss, grad};
 }
@@ -152,17 +158,17 @@ LossGrad mlp_loss_grad(const NdBuffer& params, const std::vector<FlatSegment>& s
     return out;
 }
 
-Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name) {
+Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute compute) {
     Kernel k;
     k.name = std::move(name);
     k.arity = 2;
     k.reads = {block.params};
     const std::vector<FlatSegment> segs = block.segments;
     const std::uint64_t grads_id = block.grads.id();
-    k.device_fn = [segs, grads_id](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
+    k.device_fn = [segs, grads_id, compute](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
         const DevBuffer& params = ctx.device_replica(0);
         Checked c = check_operands(params, segs, in[0], in[1]);
-        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1]);
+        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute);
         DeviceKernelResult r;
         r.outputs.push_back(loss);
         r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
