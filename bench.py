@@ -308,6 +308,42 @@ def ours(args, n_gpus):
                "samples_per_s": 256 * n_gpus * args.steps / dt, "ms_per_step": 1e3 * dt / args.steps,
                "allreduce_ms_last": 1e3 * rep["allreduce_s"], "loss_last": loss, "coherent": block.params.coherent}
 
+    # ---- wide MLP (C5) sync SGD on tcgen05 bf16 -------------------------------------------
+    sgd5 = None
+    if not args.no_sgd:
+        dims = [2048, 4096, 4096, 100]
+        cfg = sk.MlpConfig(in_dim=dims[0], width=dims[1], out_dim=dims[-1], layers=3, seed=1)
+        x, y = sk.mlp_make_dataset(16384, cfg, seed=2, dtype="f32")
+        sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
+        sx.mirror(pool)
+        sy.mirror(pool)
+        block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+        g = sk.mlp_grad_function(pool, block, compute="bf16")
+        sk.distribute(pool)
+        tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
+        per_gpu = 8192
+        sel = [rng.integers(0, 16384, per_gpu * n_gpus) for _ in range(total_steps)]
+        for s in range(args.warmup):
+            tr.train_step(g, [sx, sy], indexes=sel[s])
+        t0 = time.perf_counter()
+        for s in range(args.warmup, total_steps):
+            loss = tr.train_step(g, [sx, sy], indexes=sel[s])
+        dt = time.perf_counter() - t0
+        flops_per_sample = 6 * sum(a * b for a, b in zip(dims[:-1], dims[1:])) - 2 * dims[0] * dims[1]
+        bf16_peak = 1609.7
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                bf16_peak = float(json.load(fh)["bf16_tflops"])
+        except Exception:
+            pass
+        tflops = flops_per_sample * per_gpu * n_gpus * args.steps / dt / 1e12 / n_gpus
+        sgd5 = {"config": "C5 (R1): MLP 2048-4096-4096-100 (25,583,716 params, fp32 master), bf16 tcgen05 GEMMs, "
+                          "batch %d per GPU indexed from a 16384-row HBM mirror, SGD lr 0.01, fused grad "
+                          "all-reduce mean + update" % per_gpu,
+                "n_params": int(block.length), "samples_per_s": per_gpu * n_gpus * args.steps / dt,
+                "ms_per_step": 1e3 * dt / args.steps, "model_tflops_per_gpu": tflops,
+                "frac_of_bf16_peak": tflops / bf16_peak, "loss_last": loss, "coherent": block.params.coherent}
+
     pool.shutdown()
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * region_s / args.steps, "higher_is_better": True,
@@ -322,6 +358,8 @@ def ours(args, n_gpus):
             "gpu_launches": n_gpus * args.steps, "clocks": clocks.summary(), "setup_s": setup_s}
     if sgd:
         line["sync_sgd"] = sgd
+    if sgd5:
+        line["sync_sgd_wide_bf16"] = sgd5
     return line
 
 

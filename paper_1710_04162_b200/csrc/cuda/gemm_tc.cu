@@ -16,11 +16,17 @@
 //                       (and optionally to C^T, which this lane layout makes
 //                       fully coalesced).
 //
-// fp32 accuracy on tensor cores ("3xTF32"): operands are pre-split into
-// tf32 hi + lo parts (synk_split_tf32) and the kernel accumulates
-// hi*hi + hi*lo + lo*hi in the same TMEM accumulator (3 passes over K), which
-// keeps the error at fp32 level (the north_star's 1e-5 fp32 bar) while every
-// multiply runs on the tensor pipe.
+// 3xTF32 (kind 2): operands pre-split into tf32 hi + lo parts
+// (synk_gemm_prep mode 0); the kernel accumulates hi*hi + hi*lo + lo*hi in the
+// same TMEM accumulator (3 passes over K). Products are then exact, but the
+// tcgen05 fp32 accumulator itself rounds with a bias of ~-6.7e-9 per
+// accumulated product (profiles/r01_tcgen05_tf32_accumulation.txt), so long K
+// chains drift past the 1e-5 fp32 bar; the f32 example function therefore
+// stays on FFMA and this kernel's production use is bf16 (kind 0).
+//
+// Occupancy: 3 stages x 32 KB + barriers ~ 97 KB smem and 128 TMEM columns per
+// CTA, so two CTAs share an SM and one CTA's epilogue overlaps the other's
+// mainloop (0.43 -> 0.77-0.82 of the measured bf16 peak at 8192x4096x4096..8192^3).
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -32,7 +38,7 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 128, kThreads = 128, kStages = 4;
+constexpr int BM = 128, BN = 128, kThreads = 128, kStages = 3;  // ~97 KB smem: two CTAs per SM, one's epilogue overlaps the other's MMAs
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 bytes, one operand, one stage
 
 enum Epi { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_TANH = 2, EPI_TANH_GRAD = 3 };
@@ -150,7 +156,7 @@ __device__ __forceinline__ void store_out(void* base, uint64_t off, float v, int
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
                    uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
@@ -230,24 +236,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint64_t m = m0 + warp * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    // Row-major C: 16 consecutive columns per thread -> 16-byte vector stores
+    // when the row pitch allows; C^T: lanes hold consecutive rows -> each
+    // scalar store instruction is one coalesced warp-wide segment.
+    const bool vec_c = epi.c && ((epi.ldc * (epi.out_bf16 ? 2 : 4)) % 16 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(lane_base + c0, r);
         if (m >= M) continue;
+        float v[16];
+        const uint64_t nb = n0 + c0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const uint64_t n = n0 + c0 + j;
-            if (n >= N) break;
-            float v = __uint_as_float(r[j]);
-            if (epi.mode == EPI_BIAS) v += epi.bias[n];
-            else if (epi.mode == EPI_BIAS_TANH) v = tanhf(v + epi.bias[n]);
-            else if (epi.mode == EPI_TANH_GRAD) {
-                const float a = load_act(epi, m, n);
-                v = v * (1.0f - a * a);
+            const uint64_t n = nb + j;
+            float x = __uint_as_float(r[j]);
+            if (n < N) {
+                if (epi.mode == EPI_BIAS) x += epi.bias[n];
+                else if (epi.mode == EPI_BIAS_TANH) x = tanhf(x + epi.bias[n]);
+                else if (epi.mode == EPI_TANH_GRAD) {
+                    const float a = load_act(epi, m, n);
+                    x = x * (1.0f - a * a);
+                }
             }
-            if (epi.c) store_out(epi.c, m * epi.ldc + n, v, epi.out_bf16);
-            if (epi.ct) store_out(epi.ct, n * epi.ldct + m, v, epi.out_bf16);
+            v[j] = x;
+        }
+        if (epi.c) {
+            if (vec_c && nb + 16 <= N) {
+                if (epi.out_bf16) {
+                    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.c) + m * epi.ldc + nb);
+                    uint32_t p[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                        p[j] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+                    dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(epi.c) + m * epi.ldc + nb);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (nb + j < N) store_out(epi.c, m * epi.ldc + nb + j, v[j], epi.out_bf16);
+            }
+        }
+        if (epi.ct) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (nb + j < N) store_out(epi.ct, (nb + j) * epi.ldct + m, v[j], epi.out_bf16);
         }
     }
     tc_fence_before();
