@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--batches", type=int, default=64, help="4096-row batches gathered per launch (per step)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sgd", action="store_true")
+    p.add_argument("--dry-run", action="store_true",
+                   help="exercise only the launch/rank coordination (no GPU work); used by CPU tests")
     return p.parse_args()
 
 
@@ -282,6 +284,14 @@ def ours(args, n_gpus):
     e2e_s = time.perf_counter() - t0
     assert float(cnt) == n_step * n_gpus
     e2e = bytes_step * args.steps / e2e_s / 1e9
+    # where the e2e time goes (untimed repeat with the call report)
+    rep_acc = {"scatter_s": 0.0, "reduce_s": 0.0, "total_s": 0.0, "compute_s": 0.0}
+    for s in range(args.warmup, total_steps):
+        _, rep = f.call_with_report([arr], indexes=e2e_idx[s])
+        for k in ("scatter_s", "reduce_s", "total_s"):
+            rep_acc[k] += rep[k] / args.steps
+        rep_acc["compute_s"] += max(rep["rank_compute_s"]) / args.steps
+    e2e_breakdown = {k + "_us": 1e6 * v for k, v in rep_acc.items()}
 
     # ---- sync SGD (C1) sub-measurement ------------------------------------------------
     sgd = None
@@ -350,7 +360,8 @@ def ours(args, n_gpus):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, n_gpus),
             "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 8 * n_step * n_gpus,
-                    "d2h_bytes_per_step": 8, "path": "Function.call(indexes) -> row_count kernel -> Sum"},
+                    "d2h_bytes_per_step": 8, "path": "Function.call(indexes) -> row_count kernel -> Sum",
+                    "breakdown_per_call": e2e_breakdown},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                          "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
@@ -368,7 +379,18 @@ def main():
     rank, world, dist = dist_setup()
     n_gpus = max(args.gpus, world)
     line = None
-    if rank == 0:
+    if args.dry_run:
+        # Coordination only: every rank reports in, rank 0 alone prints.
+        if dist is not None:
+            import torch
+
+            seen = [None] * world
+            dist.all_gather_object(seen, {"rank": rank, "pid": os.getpid()})
+        else:
+            seen = [{"rank": 0, "pid": os.getpid()}]
+        line = {"metric": METRIC, "dry_run": True, "n_gpus": n_gpus, "world": world,
+                "ranks_seen": sorted(s["rank"] for s in seen), "driver_rank": 0}
+    elif rank == 0:
         if args.impl == "reference":
             line = reference_arm(args, n_gpus)
         else:

@@ -153,6 +153,9 @@ int synk_all_finite(synk_dev* dev, int dtype, const void* x, uint64_t n, int* fi
  * into chunk r of every replica: bitwise equal to ReplicatedVariable::
  * all_reduce (replicated.cpp:124-137). */
 int synk_all_reduce(synk_dev* dev, int world, int dtype, int op, void* const* bufs, uint64_t n);
+/* The element range [lo, hi) rank r owns in every collective above (host-only;
+ * 16-element aligned chunks, the last ones possibly short or empty). */
+int synk_chunk_range(uint64_t n, int world, int rank, uint64_t* lo, uint64_t* hi);
 /* Fold of all replicas into `out` (tree order), run by one rank
  * (ReplicatedVariable::reduce, replicated.cpp:139-149). */
 int synk_tree_reduce(synk_dev* dev, int world, int dtype, int op, const void* const* bufs,

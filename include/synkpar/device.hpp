@@ -47,6 +47,9 @@ public:
     int device() const noexcept;
     bool has_storage() const noexcept { return store_ != nullptr; }
     bool shares_storage(const DevBuffer& o) const noexcept { return store_ && store_ == o.store_; }
+    // True when this handle is the only reference to its storage (no view or
+    // replica can observe a write through it).
+    bool sole_owner() const noexcept { return store_ && store_.use_count() == 1; }
     const std::shared_ptr<detail::RankDevice>& owner() const;
 
     DevBuffer slice_rows(RowRange range) const;                 // zero-copy

@@ -158,13 +158,69 @@ __global__ void __launch_bounds__(kBlock) bcast_chunk_kernel(Ptrs bufs, int w, i
 }
 
 // ---- fused gradient all-reduce + optimizer update ------------------------------
+// Vector body: one 16-byte vector (4 f32 / 2 f64 elements) of chunk r per
+// iteration: W peer loads of the gradient, per-lane tree fold + 1/W, then the
+// update on this rank's (coherent) params/aux and W peer stores of each.
+// With W == 1 the fold is the identity (and x*1.0 is exact), so the gradient
+// is not rewritten.
+template <class T, int W>
+__device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
+                                            int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
+                                            int naux, uint64_t v) {
+    using V = typename V16<T>::V;
+    constexpr int N = V16<T>::N;
+    V gx[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) gx[q] = static_cast<const V*>(grads.p[q])[v];
+    V g;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        T e[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) e[q] = reinterpret_cast<const T*>(&gx[q])[k];
+        reinterpret_cast<T*>(&g)[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
+    }
+    if constexpr (W > 1) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) static_cast<V*>(grads.p[q])[v] = g;
+    }
+    V p = static_cast<const V*>(params.p[rank])[v];
+    V a0 = naux > 0 ? static_cast<const V*>(aux0.p[rank])[v] : p;
+    V a1 = naux > 1 ? static_cast<const V*>(aux1.p[rank])[v] : p;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        double pd = (double)reinterpret_cast<T*>(&p)[k];
+        double x0 = (double)reinterpret_cast<T*>(&a0)[k];
+        double x1 = (double)reinterpret_cast<T*>(&a1)[k];
+        synk::rule_update(rp, pd, x0, x1, (double)reinterpret_cast<T*>(&g)[k]);
+        reinterpret_cast<T*>(&p)[k] = (T)pd;
+        reinterpret_cast<T*>(&a0)[k] = (T)x0;
+        reinterpret_cast<T*>(&a1)[k] = (T)x1;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+        static_cast<V*>(params.p[q])[v] = p;
+        if (naux > 0) static_cast<V*>(aux0.p[q])[v] = a0;
+        if (naux > 1) static_cast<V*>(aux1.p[q])[v] = a1;
+    }
+}
+
 template <class T, int W>
 __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
-    double inv_w, synk::RuleParams rp, int naux, bool coherent, uint64_t lo, uint64_t hi) {
+    double inv_w, synk::RuleParams rp, int naux, bool coherent, uint64_t lo, uint64_t hi, bool vec) {
     const int fop = grad_op == SYNK_OP_MEAN ? SYNK_OP_SUM : grad_op;
     uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     uint64_t stride = (uint64_t)gridDim.x * kBlock;
+    if constexpr (W > 0) {
+        if (vec && coherent) {
+            constexpr int N = V16<T>::N;
+            const uint64_t v0 = lo / N, v1 = hi / N;  // lo is 16-element aligned
+            for (uint64_t v = v0 + tid; v < v1; v += stride)
+                step_vector<T, W>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v);
+            lo = v1 * N;  // scalar tail below
+        }
+    }
     for (uint64_t i = lo + tid; i < hi; i += stride) {
         T e[W > 0 ? W : kMaxWorld];
         T g;
@@ -291,18 +347,21 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     chunk_of(n, w, d->rank, &lo, &hi);
     if (lo >= hi) return SYNK_OK;
     double inv_w = 1.0 / (double)w;
-    unsigned grid = synk::grid_for(d, hi - lo, kBlock);
+    bool vec = ptrs_aligned16(params, w) && ptrs_aligned16(grads, w) && (naux < 1 || ptrs_aligned16(aux0, w)) &&
+               (naux < 2 || ptrs_aligned16(aux1, w));
+    unsigned grid = synk::grid_for(d, vec ? (hi - lo) / V16<T>::N + 1 : hi - lo, kBlock);
     switch (w) {
 #define SYNK_ARS_CASE(WW)                                                                        \
     case WW:                                                                                     \
         allreduce_step_kernel<T, WW><<<grid, kBlock, 0, d->stream>>>(                            \
-            P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi);               \
+            P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec);          \
         break;
-        SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(4) SYNK_ARS_CASE(8)
+        SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(3) SYNK_ARS_CASE(4)
+        SYNK_ARS_CASE(5) SYNK_ARS_CASE(6) SYNK_ARS_CASE(7) SYNK_ARS_CASE(8)
 #undef SYNK_ARS_CASE
     default:
         allreduce_step_kernel<T, 0><<<grid, kBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
-                                                                    inv_w, rp, naux, coherent, lo, hi);
+                                                                    inv_w, rp, naux, coherent, lo, hi, false);
     }
     SYNK_LAUNCHED("allreduce_step_kernel");
     return SYNK_OK;
@@ -332,6 +391,12 @@ int make_rule(int rule, const double* hyper, double lr, uint64_t t, synk::RulePa
 }  // namespace
 
 extern "C" {
+
+int synk_chunk_range(uint64_t n, int world, int rank, uint64_t* lo, uint64_t* hi) {
+    SYNK_REQUIRE(world >= 1 && rank >= 0 && rank < world, SYNK_EARG, "chunk_range: rank out of range");
+    chunk_of(n, world, rank, lo, hi);
+    return SYNK_OK;
+}
 
 int synk_all_reduce(synk_dev* d, int world, int dtype, int op, void* const* bufs, uint64_t n) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_all_reduce: bad dtype");

@@ -32,13 +32,15 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "common.cuh"
 
 namespace {
 
-constexpr int BM = 128, BN = 128, kThreads = 128, kStages = 3;  // ~97 KB smem: two CTAs per SM, one's epilogue overlaps the other's MMAs
+constexpr int BM = 128, BN = 128, kStages = 3;  // ~97 KB smem: two CTAs per SM, one's epilogue overlaps the other's MMAs
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 bytes, one operand, one stage
 
 enum Epi { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_TANH = 2, EPI_TANH_GRAD = 3 };
@@ -155,8 +157,8 @@ __device__ __forceinline__ void store_out(void* base, uint64_t off, float v, int
     else static_cast<float*>(base)[off] = v;
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
+__global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
                    uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
@@ -234,20 +236,50 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ---- epilogue: TMEM -> registers -> fused elementwise -> HBM ----
     mbar_wait(smem_u32(&bars[2 * kStages]), 0);
     tc_fence_after();
-    const uint64_t m = m0 + warp * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    // 8 epilogue warps: warp w reads TMEM lane quadrant w % 4 (hardware rule)
+    // and column half w / 4, so twice the memory-level parallelism of one
+    // warpgroup while the other CTA on the SM keeps the tensor pipe busy.
+    constexpr int kGroups = NT / 128, kCols = BN / kGroups;
+    const int quad = warp % 4, grp = warp / 4;
+    const uint64_t m = m0 + quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     // Row-major C: 16 consecutive columns per thread -> 16-byte vector stores
     // when the row pitch allows; C^T: lanes hold consecutive rows -> each
     // scalar store instruction is one coalesced warp-wide segment.
-    const bool vec_c = epi.c && ((epi.ldc * (epi.out_bf16 ? 2 : 4)) % 16 == 0) &&
-                       ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
+    const int es = epi.out_bf16 ? 2 : 4;
+    const bool vec_c = epi.c && ((epi.ldc * es) % 16 == 0) && ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
+    const bool vec_act = epi.mode == EPI_TANH_GRAD && ((epi.ldact * es) % 16 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(epi.act) & 15) == 0);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = grp * kCols; c0 < (grp + 1) * kCols; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(lane_base + c0, r);
         if (m >= M) continue;
         float v[16];
         const uint64_t nb = n0 + c0;
+        float act[16];
+        if (epi.mode == EPI_TANH_GRAD) {
+            if (vec_act && nb + 16 <= N) {  // 16 activations in one or two 16-byte loads
+                if (epi.out_bf16) {
+                    const uint4* src =
+                        reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact + nb);
+                    uint4 u[2] = {src[0], src[1]};
+                    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(u);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) act[j] = __bfloat162float(h[j]);
+                } else {
+                    const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(epi.act) + m * epi.ldact + nb);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float4 f = src[j];
+                        act[4 * j] = f.x, act[4 * j + 1] = f.y, act[4 * j + 2] = f.z, act[4 * j + 3] = f.w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) act[j] = nb + j < N ? load_act(epi, m, nb + j) : 0.f;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const uint64_t n = nb + j;
@@ -255,10 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (n < N) {
                 if (epi.mode == EPI_BIAS) x += epi.bias[n];
                 else if (epi.mode == EPI_BIAS_TANH) x = tanhf(x + epi.bias[n]);
-                else if (epi.mode == EPI_TANH_GRAD) {
-                    const float a = load_act(epi, m, n);
-                    x = x * (1.0f - a * a);
-                }
+                else if (epi.mode == EPI_TANH_GRAD) x = x * (1.0f - act[j] * act[j]);
             }
             v[j] = x;
         }
@@ -341,14 +370,31 @@ constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e) {
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[KIND]) {
-        SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-        attr_set[KIND] = true;
-    }
+    static bool attr_set[2][2] = {{false, false}, {false, false}};
+    // Epilogue-heavy launches (short K, or the tanh-derivative reading the
+    // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
+    // the full register budget. SYNK_GEMM_WARPS=4|8 overrides (A/B runs).
+    static const int forced = [] {
+        const char* e = getenv("SYNK_GEMM_WARPS");
+        return e ? atoi(e) : 0;
+    }();
+    const bool wide = forced ? forced == 8 : (K <= 512 || e.mode == EPI_TANH_GRAD);
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-    gemm_tc_kernel<KIND><<<grid, kThreads, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                   (uint32_t)K, e);
+    if (wide) {
+        if (!attr_set[KIND][1]) {
+            SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+            attr_set[KIND][1] = true;
+        }
+        gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
+                                                                       (uint32_t)K, e);
+    } else {
+        if (!attr_set[KIND][0]) {
+            SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+            attr_set[KIND][0] = true;
+        }
+        gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
+                                                                       (uint32_t)K, e);
+    }
     SYNK_LAUNCHED("gemm_tc_kernel");
     return SYNK_OK;
 }

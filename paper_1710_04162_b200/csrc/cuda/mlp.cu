@@ -367,8 +367,8 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         return rc;
     if (int rc = synk_gemm_prep(d, F32, delta_f, n, dl, dl, 1, 1, bf(B.off_dT[cur]), nullptr, dl, n, pad8(n)); rc)
         return rc;
-    bias_grad_kernel<float><<<(unsigned)((dl + 31) / 32), kThreads, 0, d->stream>>>(delta_f, n, dl, grad + P.boff[L - 1]);
-    SYNK_LAUNCHED("bias_grad_kernel");
+    // output-layer bias grad: row-chunked column sums (f64 accumulation), enough CTAs for large n
+    if (int rc = synk_column_stats(d, F32, delta_f, n, dl, grad + P.boff[L - 1], nullptr, nullptr); rc) return rc;
 
     // backward
     for (uint32_t l = L; l-- > 0;) {

@@ -27,7 +27,19 @@ void check(int rc, const char* what) {
 }
 
 RankDevice::~RankDevice() {
+    if (h && scratch) synk_free(h, scratch);
     if (h) synk_close(h);
+}
+
+void* rank_scratch(const std::shared_ptr<RankDevice>& rd, std::size_t bytes) {
+    if (bytes <= rd->scratch_bytes) return rd->scratch;
+    if (rd->scratch) check(synk_free(rd->h, rd->scratch), "scratch free");  // stream-ordered: after prior users
+    rd->scratch = nullptr;
+    rd->scratch_bytes = 0;
+    const std::size_t grown = bytes + bytes / 4;
+    check(synk_alloc(rd->h, grown, &rd->scratch), "scratch alloc");
+    rd->scratch_bytes = grown;
+    return rd->scratch;
 }
 
 DevStorage::~DevStorage() {

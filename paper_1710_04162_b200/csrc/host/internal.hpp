@@ -28,8 +28,17 @@ struct RankDevice {
     synk_dev* h = nullptr;
     std::size_t rank = 0;
     int device = 0;
+    // Per-rank scratch reused across calls (work on a rank is stream-ordered,
+    // so one call's kernels finish before the next call's reuse it): keeps
+    // large per-call workspaces off cudaMallocAsync, whose pool-growth path
+    // can stall the host for milliseconds.
+    void* scratch = nullptr;
+    std::size_t scratch_bytes = 0;
     ~RankDevice();
 };
+
+// Scratch of at least `bytes` on rd's device (valid until the next call that grows it).
+void* rank_scratch(const std::shared_ptr<RankDevice>& rd, std::size_t bytes);
 
 struct DevStorage {
     void* ptr = nullptr;

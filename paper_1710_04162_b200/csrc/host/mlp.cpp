@@ -84,12 +84,11 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     std::uint64_t ws_bytes = 0;
     detail::check(synk_mlp_workspace_bytes_ex(detail::synk_dtype(dt), mode, c.dims.data(), L, c.n, &ws_bytes),
                   "mlp workspace");
-    DevBuffer ws = DevBuffer::alloc(rd, {(ws_bytes + 7) / 8}, DType::Float64);
+    void* ws = detail::rank_scratch(rd, ws_bytes);
     DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
     DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
     detail::check(synk_mlp_loss_grad_ex(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
-                                        yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws.data(),
-                                        ws_bytes),
+                                        yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws, ws_bytes),
                   "mlp_loss_grad");
     return {loss, grad};
 }

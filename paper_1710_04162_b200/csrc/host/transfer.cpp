@@ -23,7 +23,7 @@ bool is_mapped_host(const void* p) {
 } // namespace
 
 DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffer& src, const DevBuffer* mirror,
-                            const std::optional<IndexSelection>& sel, RowRange part) {
+                            const std::optional<IndexSelection>& sel, RowRange part, IndexUploads* uploads) {
     const std::size_t n_src = src.rows();
     const std::size_t row_bytes = src.row_size() * dtype_size(src.dtype());
     std::vector<std::size_t> shape = src.shape();
@@ -46,7 +46,15 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     if (part.stop > list.size()) throw BoundsError("excerpt_rows(): part extends past the index list");
     DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
     if (part.count() == 0 || row_bytes == 0) return out;
-    DevBuffer idx = upload_indices(rd, list.data() + part.start, part.count());
+    const std::pair<const std::size_t*, std::size_t> key{list.data() + part.start, part.count()};
+    DevBuffer idx;
+    if (uploads)
+        for (auto& [k, buf] : uploads->done)
+            if (k == key) idx = buf;
+    if (!idx.has_storage()) {
+        idx = upload_indices(rd, key.first, key.second);
+        if (uploads) uploads->done.emplace_back(key, idx);
+    }
 
     const void* base = nullptr;
     DevBuffer staged;  // keeps a device copy alive when the host source is pageable

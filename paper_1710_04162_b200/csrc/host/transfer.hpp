@@ -14,8 +14,14 @@ namespace synkpar::detail {
 // Rows `part` of the (optionally selected) rows of host array `src`, on rank
 // `rd`'s GPU. `mirror` is the device copy of src's storage on that GPU (or
 // nullptr), addressed like src.bytes().
+// Index lists already uploaded during one rank task (scatter arguments of a
+// call share one selection: upload it once).
+struct IndexUploads {
+    std::vector<std::pair<std::pair<const std::size_t*, std::size_t>, DevBuffer>> done;
+};
+
 DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffer& src, const DevBuffer* mirror,
-                            const std::optional<IndexSelection>& sel, RowRange part);
+                            const std::optional<IndexSelection>& sel, RowRange part, IndexUploads* uploads = nullptr);
 
 // Rows of a device buffer picked by `sel` (RowRange -> view, IndexList -> gather kernel).
 DevBuffer select_device_rows(const std::shared_ptr<RankDevice>& rd, const DevBuffer& src,
