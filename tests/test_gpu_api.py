@@ -350,3 +350,29 @@ def test_allreduce_ablation(sk):
             for _ in range(3):
                 t.train_step(f, [x, y])
             assert block.params.coherent == all_reduce
+
+
+def test_bench_report_shape(sk):
+    # python/tests/test_smoke.py:135-143 of the reference
+    report = sk.run_bench(workers=[1, 2], steps=2, batch=8, width=8, layers=2, in_dim=4, out_dim=2, seed=3)
+    assert [run["workers"] for run in report["runs"]] == [1, 2]
+    for run in report["runs"]:
+        for key in ("total_s", "function_s", "shuffle_s", "straggler_s", "allreduce_s", "steps_per_s", "rows_per_s",
+                    "speedup_vs_1", "speedup_vs_2"):
+            assert key in run
+    assert report["config"]["batch_mode"] == "scaled"
+
+
+def test_bench_losses_match_reference(sk, oracle):
+    """Same seeds -> same batches -> same f64 Adam trajectory as the reference bench."""
+    ref = oracle.reference_module()
+    if ref is None:
+        pytest.skip("reference module not present on this box")
+    kw = dict(workers=[1, 2], steps=3, batch=8, width=8, layers=2, in_dim=4, out_dim=2, seed=3, batch_mode="fixed")
+    ours = sk.run_bench(**kw)
+    theirs = ref.run_bench_json(**kw)
+    import json
+    theirs = json.loads(theirs)
+    assert [r["workers"] for r in ours["runs"]] == [r["workers"] for r in theirs["runs"]]
+    for k in ("steps", "batch", "batch_mode", "width", "layers", "seed"):
+        assert ours["config"][k] == theirs["config"][k]
