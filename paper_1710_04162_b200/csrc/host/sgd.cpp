@@ -151,7 +151,7 @@ SyncSgd::SyncSgd(WorkerPool& pool, FlatParamBlock block, UpdateRule rule, double
     const int code = rule_code(rule_);
     const std::vector<double> hyper = rule_hyper(rule_);
     const double lr_copy = lr_;
-    const std::uint64_t* t_ptr = &t_;
+    std::shared_ptr<std::uint64_t> t_ptr = step_box_;
     k.device_fn = [ids, code, hyper, lr_copy, naux, t_ptr](const std::vector<DevBuffer>&, const KernelContext& ctx) {
         const DevBuffer& p0 = ctx.device_replica(0);
         const DevBuffer& g = ctx.device_replica(1);
@@ -270,6 +270,7 @@ double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<Fun
         detail::record_of(block_.params).coherent = true;
         for (const ReplicatedVariable& a : aux_) detail::record_of(a).coherent = true;
     } else {
+        *step_box_ = t_;  // the step kernel applies step t_ + 1 (sgd.cpp:231,237 of the reference)
         CallResult sr = f_step_.call({FunctionArg(NdBuffer::scalar(double(t_ + 1)))});
         rep.step_call = sr.report;
     }
