@@ -274,7 +274,14 @@ def ours(args, n_gpus):
     # ---- e2e through the public API --------------------------------------------------
     f = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
     sk.distribute(pool)
-    e2e_idx = [rng.integers(0, rows, n_step * n_gpus) for _ in range(total_steps)]
+    # Per-step index lists live in pinned host memory (sk.pinned_array): the call
+    # reads them in place and DMAs each rank's part (filled before timing, as a
+    # data loader would hand them over).
+    e2e_idx = []
+    for _ in range(total_steps):
+        buf = sk.pinned_array(n_step * n_gpus, "int64")
+        buf[:] = rng.integers(0, rows, n_step * n_gpus)
+        e2e_idx.append(buf)
     for s in range(args.warmup):
         (cnt,) = f.call([arr], indexes=e2e_idx[s])
         assert float(cnt) == n_step * n_gpus

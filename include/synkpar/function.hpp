@@ -109,6 +109,13 @@ struct CallOptions {
     std::size_t num_slices = 1;
     std::optional<IndexSelection> indexes;
     std::optional<std::vector<IndexSelection>> replica_indexes;
+    // ---- B200 addition (appended) ----
+    // A borrowed index list used instead of `indexes` when `indexes` is unset:
+    // same meaning as an IndexList of `index_view_count` entries, read in
+    // place (no copy; pinned host memory is DMA'd straight to each GPU). Must
+    // stay valid and unmodified for the duration of the call.
+    const std::uint64_t* index_view = nullptr;
+    std::size_t index_view_count = 0;
 };
 
 struct CallReport {

@@ -239,7 +239,7 @@ void ReplicatedVariable::scatter_value(const NdBuffer& data, const std::optional
     detail::PoolState& st = *rec.pool;
     detail::run_pool_phase(st, PhaseKind::ScatterVar, [&](std::size_t r) {
         // Fresh HBM storage per rank (never aliases the source, replicated.cpp:186-188).
-        rec.replicas[r] = detail::excerpt_to_device(st.ranks[r], data, nullptr, indexes, parts[r]);
+        rec.replicas[r] = detail::excerpt_to_device(st.ranks[r], data, nullptr, detail::SelView::of(indexes), parts[r]);
         detail::dev_sync(st.ranks[r]);
     });
     if (rec.replicas.size() > 1) rec.coherent = false;

@@ -6,11 +6,44 @@
 
 namespace synkpar::detail {
 
-DevBuffer upload_indices(const std::shared_ptr<RankDevice>& rd, const std::size_t* idx, std::size_t n) {
-    static_assert(sizeof(std::size_t) == sizeof(std::uint64_t), "index lists are u64 on the device");
-    DevBuffer out = DevBuffer::alloc(rd, {n}, DType::Float64);  // 8-byte slots; dtype is bookkeeping
-    if (n) check(synk_copy(rd->h, out.data(), idx, n * sizeof(std::uint64_t)), "upload indices");
-    return out;
+static_assert(sizeof(std::size_t) == sizeof(std::uint64_t), "index lists are u64 on the device");
+
+SelView SelView::of(const std::optional<IndexSelection>& sel) {
+    SelView v;
+    if (!sel) return v;
+    v.has = true;
+    if (const RowRange* r = std::get_if<RowRange>(&*sel)) {
+        v.is_range = true;
+        v.range = *r;
+    } else {
+        const IndexList& l = std::get<IndexList>(*sel);
+        v.list = reinterpret_cast<const std::uint64_t*>(l.data());
+        v.count = l.size();
+    }
+    return v;
+}
+
+SelView SelView::borrowed(const std::uint64_t* list, std::size_t count) {
+    SelView v;
+    v.has = true;
+    v.list = list;
+    v.count = count;
+    return v;
+}
+
+void validate_view(const SelView& sel, std::size_t n) {
+    if (!sel.has) return;
+    if (sel.is_range) {
+        validate_selection(IndexSelection(sel.range), n);
+        return;
+    }
+    std::uint64_t hi = 0;
+    for (std::size_t i = 0; i < sel.count; ++i) hi = sel.list[i] > hi ? sel.list[i] : hi;
+    if (sel.count == 0 || hi < n) return;
+    for (std::size_t i = 0; i < sel.count; ++i)
+        if (sel.list[i] >= n)
+            throw BoundsError("selection index " + std::to_string(sel.list[i]) + " not within " + std::to_string(n) +
+                              " rows");
 }
 
 namespace {
@@ -22,17 +55,23 @@ bool is_mapped_host(const void* p) {
 
 } // namespace
 
+DevBuffer upload_indices(const std::shared_ptr<RankDevice>& rd, const std::uint64_t* idx, std::size_t n) {
+    DevBuffer out = DevBuffer::alloc(rd, {n}, DType::Float64);  // 8-byte slots; dtype is bookkeeping
+    // Pinned sources go out as an async DMA; pageable ones are staged by the driver.
+    if (n) check(synk_copy(rd->h, out.data(), idx, n * sizeof(std::uint64_t)), "upload indices");
+    return out;
+}
+
 DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffer& src, const DevBuffer* mirror,
-                            const std::optional<IndexSelection>& sel, RowRange part, IndexUploads* uploads) {
+                            const SelView& sel, RowRange part, IndexUploads* uploads) {
     const std::size_t n_src = src.rows();
     const std::size_t row_bytes = src.row_size() * dtype_size(src.dtype());
     std::vector<std::size_t> shape = src.shape();
     shape[0] = part.count();
     const bool have_mirror = mirror && mirror->has_storage();
 
-    const RowRange* range = sel ? std::get_if<RowRange>(&*sel) : nullptr;
-    if (!sel || range) {
-        const std::size_t first = (range ? range->start : 0) + part.start;
+    if (!sel.has || sel.is_range) {
+        const std::size_t first = (sel.has ? sel.range.start : 0) + part.start;
         if (first + part.count() > n_src) throw BoundsError("excerpt: rows past the end of the source");
         if (have_mirror)  // zero-copy view of the HBM mirror
             return mirror->reinterpret(src.offset_bytes() + first * row_bytes, std::move(shape), src.dtype());
@@ -42,11 +81,10 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
         return out;
     }
 
-    const IndexList& list = std::get<IndexList>(*sel);
-    if (part.stop > list.size()) throw BoundsError("excerpt_rows(): part extends past the index list");
+    if (part.stop > sel.count) throw BoundsError("excerpt_rows(): part extends past the index list");
     DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
     if (part.count() == 0 || row_bytes == 0) return out;
-    const std::pair<const std::size_t*, std::size_t> key{list.data() + part.start, part.count()};
+    const std::pair<const std::uint64_t*, std::size_t> key{sel.list + part.start, part.count()};
     DevBuffer idx;
     if (uploads)
         for (auto& [k, buf] : uploads->done)
@@ -67,8 +105,8 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
         check(synk_copy(rd->h, staged.data(), src.bytes(), src.byte_size()), "excerpt: stage pageable source");
         base = staged.data();
     }
-    check(synk_gather_rows(rd->h, base, n_src, row_bytes, static_cast<const std::uint64_t*>(idx.data()),
-                           part.count(), out.data()),
+    check(synk_gather_rows(rd->h, base, n_src, row_bytes, static_cast<const std::uint64_t*>(idx.data()), part.count(),
+                           out.data()),
           "gather_rows");
     return out;
 }
@@ -81,7 +119,7 @@ DevBuffer select_device_rows(const std::shared_ptr<RankDevice>& rd, const DevBuf
     DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
     const std::size_t row_bytes = src.row_size() * dtype_size(src.dtype());
     if (list.empty() || row_bytes == 0) return out;
-    DevBuffer idx = upload_indices(rd, list.data(), list.size());
+    DevBuffer idx = upload_indices(rd, reinterpret_cast<const std::uint64_t*>(list.data()), list.size());
     check(synk_gather_rows(rd->h, src.data(), src.rows(), row_bytes, static_cast<const std::uint64_t*>(idx.data()),
                            list.size(), out.data()),
           "gather_rows (replica)");

@@ -129,6 +129,32 @@ def test_indexed_gather_bit_exact(sk, oracle, world):
         assert serial.tobytes() == got.tobytes()
 
 
+def test_borrowed_and_pinned_index_arrays(sk, oracle):
+    """int64/uint64 ndarrays are read in place (no IndexList copy); pinned arrays
+    are DMA'd; results identical to list indexes; validation unchanged."""
+    rng = np.random.default_rng(21)
+    src = rng.uniform(-1, 1, (3000, 64)).astype(np.float32)
+    idx = rng.integers(0, 3000, 5000)
+    pinned = sk.pinned_array(idx.size, "int64")
+    pinned[:] = idx
+    with sk.Pool(workers=3) as pool:
+        arr = sk.SharedInput.from_array(src)
+        f = sk.make_function(pool, sk.identity_kernel(), ["scatter"], ["gather"])
+        sk.distribute(pool)
+        want = oracle.gather_rows(src, idx.astype(np.uint64)).tobytes()
+        for sel in (idx, idx.astype(np.uint64), pinned, idx.tolist()):
+            (got,) = f.call([arr], indexes=sel, num_slices=2)
+            assert got.tobytes() == want
+        bad = idx.copy()
+        bad[17] = 3000
+        with pytest.raises(sk.BoundsError):
+            f.call([arr], indexes=bad)
+        bad[17] = -1
+        with pytest.raises(sk.BoundsError):
+            f.call([arr], indexes=bad)
+        assert pool.alive
+
+
 def test_gather_golden_through_api(sk):
     g = golden("gather.npz")
     for tag in ("f32", "f64"):
