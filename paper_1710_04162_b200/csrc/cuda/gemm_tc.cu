@@ -34,6 +34,7 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -157,6 +158,9 @@ __device__ __forceinline__ void store_out(void* base, uint64_t off, float v, int
     else static_cast<float*>(base)[off] = v;
 }
 
+__device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
+                                          const uint32_t (&r)[16], bool vec_c, bool vec_act);
+
 template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
 __global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
@@ -255,8 +259,23 @@ __global__ void __launch_bounds__(NT, 2)
         uint32_t r[16];
         tmem_ld16(lane_base + c0, r);
         if (m >= M) continue;
+        epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    }
+}
+
+// Fused epilogue for 16 consecutive columns [nb, nb+16) of row m, accumulator
+// values r (fp32 bits): bias / tanh / tanh-derivative, then row-major C
+// (16-byte vector stores when aligned) and/or C^T (lanes = consecutive rows,
+// so each scalar store instruction is one coalesced warp segment).
+__device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
+                                          const uint32_t (&r)[16], bool vec_c, bool vec_act) {
+    {
         float v[16];
-        const uint64_t nb = n0 + c0;
         float act[16];
         if (epi.mode == EPI_TANH_GRAD) {
             if (vec_act && nb + 16 <= N) {  // 16 activations in one or two 16-byte loads
@@ -320,11 +339,127 @@ __global__ void __launch_bounds__(NT, 2)
                 if (nb + j < N) store_out(epi.ct, (nb + j) * epi.ldct + m, v[j], epi.out_bf16);
         }
     }
+}
+
+// ---- persistent bf16 kernel: 128 x 256 tiles, double-buffered TMEM accumulators -------
+// One CTA per SM loops over tiles (static round robin). The 128x256x16 UMMA
+// reads 12 KB of operands per 128 cycles (96 B/clk, inside the 128 B/clk
+// shared-memory budget that a 128x128 tile saturates), and the two 256-column
+// accumulators let the epilogue warpgroup drain tile i while the MMA warp
+// already accumulates tile i+1.
+// 12 warps: 0 TMA, 1 MMA, 2 TMEM allocator, 3 idle, 4..11 epilogue (two warps
+// per TMEM lane quadrant, each draining half of the 256 accumulator columns).
+constexpr int PBN = 256, PStages = 4, PThreads = 384, PEpiThreads = 256;
+constexpr int PA = 128 * 128, PB = 256 * 128;  // bytes per stage: A 128 rows, B 256 rows, 128 B each
+
+__global__ void __launch_bounds__(PThreads, 1)
+    gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                              uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + PStages * PA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + PStages * PB);
+    uint64_t* full = bars;                 // [PStages]
+    uint64_t* empty = bars + PStages;      // [PStages]
+    uint64_t* tfull = bars + 2 * PStages;  // [2]
+    uint64_t* tempty = tfull + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    constexpr int kBK = 64;  // bf16 elements per 128-byte K block
+    const uint32_t num_m = (M + BM - 1) / BM, num_n = (N + PBN - 1) / PBN;
+    const uint32_t tiles = num_m * num_n;
+    const int num_kb = (int)((K + kBK - 1) / kBK);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < PStages; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&tfull[b]), 1);
+            mbar_init(smem_u32(&tempty[b]), PEpiThreads);  // every epilogue thread arrives
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_map(&ta);
+        prefetch_map(&tb);
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * PBN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (int)((t / num_n) * BM), n0 = (int)((t % num_n) * PBN);
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                const int s = it % PStages;
+                mbar_wait(smem_u32(&empty[s]), ((it / PStages) & 1) ^ 1);
+                mbar_expect_tx(smem_u32(&full[s]), PA + PB);
+                tma_load_2d(smem_u32(sa + s * PA), &ta, smem_u32(&full[s]), kb * kBK, m0);
+                tma_load_2d(smem_u32(sb + s * PB), &tb, smem_u32(&full[s]), kb * kBK, n0);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PBN >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+        uint32_t it = 0, tl = 0;
+        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl & 1;
+            mbar_wait(smem_u32(&tempty[acc]), ((tl >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            tc_fence_after();
+            const uint32_t d = tmem + acc * PBN;
+            for (int kb = 0; kb < num_kb; ++kb, ++it) {
+                const int s = it % PStages;
+                mbar_wait(smem_u32(&full[s]), (it / PStages) & 1);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(sa + s * PA), b_base = smem_u32(sb + s * PB);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    umma<0>(d, smem_desc(a_base + 32 * k), smem_desc(b_base + 32 * k), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                umma_commit(smem_u32(&empty[s]));
+            }
+            umma_commit(smem_u32(&tfull[acc]));
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue: warps 4..11; warp w owns TMEM lane quadrant w % 4 and
+        // accumulator columns [128 * half, 128 * half + 128), half = (w - 4) / 4 ----
+        const int quad = warp % 4, half = (warp - 4) / 4;
+        const int es = epi.out_bf16 ? 2 : 4;
+        const bool vec_c = epi.c && ((epi.ldc * es) % 16 == 0) && ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
+        const bool vec_act = epi.mode == EPI_TANH_GRAD && ((epi.ldact * es) % 16 == 0) &&
+                             ((reinterpret_cast<uintptr_t>(epi.act) & 15) == 0);
+        uint32_t tl = 0;
+        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl & 1;
+            const uint64_t m0 = (t / num_n) * BM, n0 = (uint64_t)(t % num_n) * PBN;
+            mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
+            tc_fence_after();
+            const uint64_t m = m0 + quad * 32 + lane;
+            const uint32_t base = tmem + acc * PBN + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+            for (int c0 = half * (PBN / 2); c0 < (half + 1) * (PBN / 2); c0 += 16) {
+                uint32_t r[16];
+                tmem_ld16(base + c0, r);
+                if (m < M && n0 + c0 < N) epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act);
+            }
+            tc_fence_before();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+        }
     }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * PBN));
 }
 
 // ---- host side: tensor maps ---------------------------------------------------------
@@ -347,7 +482,8 @@ EncodeFn encoder() {
 }
 
 // rows x k matrix, K-major with leading dimension ld (elements); box = 128 rows x 128 bytes.
-int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t ld, bool bf16) {
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t ld, bool bf16,
+             uint32_t box_rows = 128) {
     EncodeFn enc = encoder();
     SYNK_REQUIRE(enc != nullptr, SYNK_ECUDA, "cuTensorMapEncodeTiled unavailable");
     const uint64_t es = bf16 ? 2 : 4;
@@ -355,7 +491,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint
                  "gemm_tc: operand base and row pitch must be 16-byte aligned");
     cuuint64_t dims[2] = {k, rows};
     cuuint64_t strides[1] = {ld * es};
-    cuuint32_t box[2] = {(cuuint32_t)(128 / es), 128};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / es), box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -487,6 +623,26 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
     }
     EpiArgs e{epilogue, out_dtype == 3, c, ldc, ct, ldct, bias, act, ldact};
     if (K == 0) return synk::fail(SYNK_EARG, "gemm_tc: K must be > 0");
+    // Wide bf16 problems: persistent 128x256 tiles (SYNK_GEMM_PERSISTENT=0 disables).
+    static const bool persistent_ok = [] {
+        const char* v = getenv("SYNK_GEMM_PERSISTENT");
+        return !(v && v[0] == '0');
+    }();
+    if (bf16 && persistent_ok && N > 128 && K > 256) {
+        CUtensorMap bw;
+        if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
+        constexpr size_t smem = (size_t)PStages * (PA + PB) + 1024 + 256;
+        static bool attr = false;
+        if (!attr) {
+            SYNK_CU(cudaFuncSetAttribute(gemm_tc_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        const uint64_t tiles = ((M + BM - 1) / BM) * ((N + PBN - 1) / PBN);
+        const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
+        gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e);
+        SYNK_LAUNCHED("gemm_tc_persistent_kernel");
+        return SYNK_OK;
+    }
     return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e)
                 : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, e);
 }

@@ -91,6 +91,29 @@ def test_single_pass_kinds(kind, tol):
     assert rel_err(got, want) > 0  # it really ran at reduced precision
 
 
+def bf16_round(x):
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16  # round-to-nearest-even to bf16
+    return u.astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 2048, 512), (1000, 4000, 600), (8192, 384, 2048)])
+def test_bf16_persistent_many_tiles(M, N, K):
+    """Shapes that take the persistent 128x256 path with more tiles than SMs
+    (both TMEM accumulators cycle) and ragged edges; exact products of
+    bf16-rounded inputs, so the only error is fp32 accumulation."""
+    rng = np.random.default_rng(M + N + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)))
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        got, got_t = gemm(R, "bf16", a, b, want_t=True)
+    # accumulator rounding only (~7e-9 x K relative to the running partial sums,
+    # whose magnitude can exceed the final value): bugs show up as O(1) errors
+    assert rel_err(got, want) <= 1e-6 + 5e-8 * K
+    np.testing.assert_array_equal(got_t, got.T)
+
+
 def test_fused_epilogues():
     rng = np.random.default_rng(2)
     M, N, K = 192, 160, 256
