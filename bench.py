@@ -69,6 +69,25 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(bytes_per_launch, path="profiles/r01_gather_ncu_full_raw.csv"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the committed
+    `ncu --set full` capture of the same gather launch (same rows per launch),
+    or None when the capture does not match this launch size."""
+    try:
+        vals = {}
+        with open(os.path.join(ROOT, path)) as fh:
+            for line in fh:
+                f = line.strip().split(",")
+                if len(f) == 3:
+                    vals[f[0]] = (f[1], f[2])
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        total = sum(float(vals[k][1]) * scale[vals[k][0]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        captured = float(vals.get("synk__algorithmic_bytes_per_launch", ("", "538968064"))[1])
+        return total if abs(captured - bytes_per_launch) < 1 else None
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -370,7 +389,8 @@ def ours(args, n_gpus):
                     "d2h_bytes_per_step": 8, "path": "Function.call(indexes) -> row_count kernel -> Sum",
                     "breakdown_per_call": e2e_breakdown},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": ncu_traffic(n_step * (2 * row_bytes + 8)),
+                         "traffic_unit": "bytes/launch", "peak_kind": peak_kind,
                          "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
             "single_batch_us": 1e6 * single_s,
             "gpu_launches": n_gpus * args.steps, "clocks": clocks.summary(), "setup_s": setup_s}
