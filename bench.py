@@ -55,6 +55,10 @@ def parse():
     p.add_argument("--batches", type=int, default=64, help="4096-row batches gathered per launch (per step)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sgd", action="store_true")
+    p.add_argument("--no-c3", action="store_true", help="skip the C3 slicing/aggregation sub-measurement")
+    p.add_argument("--c3-rows", type=int, default=8_388_608)
+    p.add_argument("--c3-cols", type=int, default=1024)
+    p.add_argument("--c3-slices", type=int, default=4)
     p.add_argument("--dry-run", action="store_true",
                    help="exercise only the launch/rank coordination (no GPU work); used by CPU tests")
     return p.parse_args()
@@ -200,6 +204,61 @@ def fill_dataset(sk, rows, cols):
         n = min(block, rows - r0)
         arr.write(r0, r0 + n, rng.random((n, cols), dtype=np.float32) * 2 - 1)
     return arr
+
+
+def slicing_c3(sk, pool, args, n_gpus, peak, peak_kind):
+    """C3: column sums (Sum) + column maxima (Max) + the shard (Gather) over an
+    HBM-resident rows x cols f32 input scattered over the GPUs, num_slices
+    slices per rank. Algorithmic bytes = one read of the input (4*rows*cols);
+    the Gather output additionally crosses PCIe to the host result."""
+    rows, cols, slices = args.c3_rows, args.c3_cols, args.c3_slices
+    nbytes = rows * cols * 4
+    t0 = time.time()
+    x = sk.replicate(pool, np.zeros(1, np.float32))
+    x.scatter_uniform([rows, cols], "f32", 3)
+    gen_s = time.time() - t0
+    f_red = sk.make_function(pool, sk.column_stats_kernel(with_shard=False), ["scatter"], ["sum", "max"])
+    f_all = sk.make_function(pool, sk.column_stats_kernel(), ["scatter"], ["sum", "max", "gather"])
+    sk.distribute(pool)
+
+    def run(f, warm, steps):
+        for _ in range(warm):
+            f.call([x], num_slices=slices)
+        dev, host = [], 0.0
+        for _ in range(steps):
+            t = time.perf_counter()
+            outs, rep = f.call_with_report([x], num_slices=slices)
+            host += time.perf_counter() - t
+            dev.append(max(rep["rank_compute_s"]))
+            del outs
+        return host / steps, float(np.mean(dev)), rep
+
+    red_host, red_dev, _ = run(f_red, 3, 10)
+    all_host, all_dev, rep = run(f_all, 2, 3)
+    per_gpu = nbytes / n_gpus
+    out = {"config": "C3: %dx%d f32 (%.1f GiB) HBM-resident (scatter_uniform), num_slices=%d per rank, "
+                     "column_stats kernel (Sum, Max[, Gather])" % (rows, cols, nbytes / 2**30, slices),
+           "algorithmic_bytes_per_call": nbytes,
+           "reduce_only": {"outputs": "sum, max", "ms_per_call": 1e3 * red_host,
+                           "e2e_gbs": nbytes / red_host / 1e9, "device_gbs": nbytes / red_dev / 1e9,
+                           "roofline": {"bound": "hbm", "achieved": per_gpu / red_dev / 1e9, "peak": peak,
+                                        "unit": "GB/s", "frac": per_gpu / red_dev / 1e9 / peak, "peak_kind": peak_kind,
+                                        "kernel": "colstats_partial_kernel + colstats_final_kernel (4 slices)"}},
+           "with_gather": {"outputs": "sum, max, gather", "ms_per_call": 1e3 * all_host,
+                           "e2e_gbs": nbytes / all_host / 1e9, "device_gbs": nbytes / all_dev / 1e9,
+                           "d2h_bytes_per_call": nbytes, "reduce_s": rep["reduce_s"],
+                           "note": "e2e bound by the %.1f GiB Gather result crossing PCIe into a pinned host "
+                                   "buffer" % (nbytes / 2**30)},
+           "generate_s": gen_s}
+    if not args.no_cpu_baseline and n_gpus >= 1:
+        sample = 262144
+        res, err = run_reference_driver("slicing", ["--rows", sample, "--cols", cols, "--slices", slices,
+                                                    "--steps", 2, "--warmup", 1, "--workers", os.cpu_count() or 1])
+        out["cpu_baseline"] = err and {"unavailable": err} or {
+            "value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
+            "sample": "2 calls over %dx%d f32 (explicit scatter input), num_slices=%d, Sum+Max+Gather" % (
+                sample, cols, slices)}
+    return out
 
 
 def ours(args, n_gpus):
@@ -380,6 +439,11 @@ def ours(args, n_gpus):
                 "ms_per_step": 1e3 * dt / args.steps, "model_tflops_per_gpu": tflops,
                 "frac_of_bf16_peak": tflops / bf16_peak, "loss_last": loss, "coherent": block.params.coherent}
 
+    # ---- slicing + aggregation (C3) sub-measurement ----------------------------------
+    c3 = None
+    if not args.no_c3:
+        c3 = slicing_c3(sk, pool, args, n_gpus, peak, peak_kind)
+
     pool.shutdown()
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * region_s / args.steps, "higher_is_better": True,
@@ -398,6 +462,8 @@ def ours(args, n_gpus):
         line["sync_sgd"] = sgd
     if sgd5:
         line["sync_sgd_wide_bf16"] = sgd5
+    if c3:
+        line["slicing_c3"] = c3
     return line
 
 

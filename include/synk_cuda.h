@@ -109,6 +109,12 @@ int synk_copy2d(synk_dev* dev, void* dst, uint64_t dpitch, const void* src, uint
 int synk_memset(synk_dev* dev, void* dst, int value, uint64_t bytes);
 /* Fill n elements with a value (NdBuffer::fill, tensor.cpp:141-151). */
 int synk_fill(synk_dev* dev, int dtype, void* dst, double value, uint64_t n);
+/* Synthetic data generated in place (no reference counterpart: replaces the
+ * host-side dataset generation + H2D of bench.cpp:41-58 / acceptance C3 for
+ * HBM-resident inputs). Element i of dst = U[-1,1) value number first+i of
+ * the stream `seed`: splitmix64(seed + (first+i)*0x9E3779B97F4A7C15) >> 40,
+ * times 2^-23, minus 1 (exact in f32 and f64; oracle: so_fill_uniform). */
+int synk_fill_uniform(synk_dev* dev, int dtype, void* dst, uint64_t n, uint64_t seed, uint64_t first);
 
 /* dst = (dst dtype) src, elementwise (NdBuffer::get/set conversions). */
 int synk_cast(synk_dev* dev, int dst_dtype, void* dst, int src_dtype, const void* src, uint64_t n);

@@ -179,6 +179,7 @@ Kernel identity_kernel(std::string name = "identity");
 Kernel row_count_kernel(std::string name = "row_count");
 // "column_stats": outputs column sum, column max, and the shard itself, for
 // (Sum, Max, Gather) -- the slicing/aggregation config of the benchmark.
-Kernel column_stats_kernel(std::string name = "column_stats");
+// with_shard=false drops the third output (declare only Sum, Max).
+Kernel column_stats_kernel(std::string name = "column_stats", bool with_shard = true);
 
 } // namespace synkpar

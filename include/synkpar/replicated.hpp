@@ -52,6 +52,11 @@ public:
     // ---- B200 additions ----
     // Rank r's replica in HBM (aliases the replica; read-only by contract).
     DevBuffer device_value(std::size_t rank) const;
+    // scatter_value() of a synthetic dataset generated in HBM: the virtual
+    // array of `shape` whose element i is synk_fill_uniform's value i of
+    // stream `seed`; rank r receives rows partition_rows(shape[0], W)[r].
+    // No host copy (HBM-resident inputs).
+    void scatter_uniform(const std::vector<std::size_t>& shape, DType dtype, std::uint64_t seed);
 
 private:
     friend std::vector<DevBuffer>& detail::replicas_of(const ReplicatedVariable&);

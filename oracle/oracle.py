@@ -181,6 +181,13 @@ def column_fold(x, kind):
     return out
 
 
+def fill_uniform(n, seed, first=0, dtype=np.float32):
+    """Synthetic U[-1,1) stream (synk_fill_uniform's formula)."""
+    out = np.empty(n, dtype)
+    _lib().so_fill_uniform(_dt(out), _p(out), ctypes.c_uint64(n), ctypes.c_uint64(seed), ctypes.c_uint64(first))
+    return out
+
+
 def elem_err(a, b):
     """support.hpp:17-30: max |a-b| / max(1, |b|)."""
     a = np.asarray(a, np.float64)

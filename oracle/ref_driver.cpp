@@ -9,6 +9,11 @@
 //           gather_rows.
 //   sgd:    SyncSgd::train_step of the MLP (in-width-out, layers 2) on a
 //           SharedInputArray dataset, indexed batches (C1).
+//   slicing: ParallelFunction over an explicit scatter input [rows x cols]
+//           f32 with num_slices slices; the kernel returns column sums (Sum),
+//           column maxima (Max) and the shard itself (Gather) -- the
+//           acceptance battery's columnwise kernels (acceptance_main.cpp:86-133)
+//           written over spans (C3).
 //
 // Prints one JSON object on stdout.
 
@@ -16,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <random>
 #include <string>
 #include <thread>
@@ -154,11 +160,66 @@ static int run_sgd(int argc, char** argv) {
     return 0;
 }
 
+static int run_slicing(int argc, char** argv) {
+    const std::size_t rows = arg(argc, argv, "--rows", 262144), cols = arg(argc, argv, "--cols", 1024);
+    const std::size_t slices = arg(argc, argv, "--slices", 4);
+    const long steps = arg(argc, argv, "--steps", 3), warmup = arg(argc, argv, "--warmup", 1);
+    std::size_t workers = arg(argc, argv, "--workers", 0);
+    if (workers == 0) workers = std::max(1u, std::thread::hardware_concurrency());
+    NdBuffer x = NdBuffer::zeros({rows, cols}, DType::Float32);
+    {
+        std::uint64_t s = 7;
+        for (float& v : x.as_mut<float>()) v = float(double(splitmix(s) >> 11) * (2.0 / 9007199254740992.0) - 1.0);
+    }
+    WorkerPool pool = WorkerPool::fork(ForkOptions{.workers = workers, .pin_threads = true});
+    Kernel k;
+    k.name = "column_stats";
+    k.arity = 1;
+    k.fn = [](const std::vector<NdBuffer>& in, const KernelContext&) {
+        const NdBuffer& a = in[0];
+        const std::size_t c = a.row_size();
+        NdBuffer sum = NdBuffer::zeros({c}, a.dtype());
+        NdBuffer mx = NdBuffer::full({c}, -std::numeric_limits<double>::infinity(), a.dtype());
+        auto v = a.as<float>();
+        auto so = sum.as_mut<float>();
+        auto mo = mx.as_mut<float>();
+        for (std::size_t r = 0; r < a.rows(); ++r)
+            for (std::size_t j = 0; j < c; ++j) {
+                const float e = v[r * c + j];
+                so[j] += e;
+                mo[j] = e > mo[j] ? e : mo[j];
+            }
+        return KernelResult{{sum, mx, a}, {}};
+    };
+    ParallelFunction f = function(pool, k, {InputSpec{InputMode::Scatter}},
+                                  {OutputSpec{ReduceOp::Sum}, OutputSpec{ReduceOp::Max}, OutputSpec{ReduceOp::Gather}});
+    distribute(pool);
+    double timed = 0.0;
+    for (long s = 0; s < warmup + steps; ++s) {
+        CallOptions o;
+        o.num_slices = slices;
+        auto t0 = Clock::now();
+        CallResult r = f.call({FunctionArg(x)}, o);
+        double d = std::chrono::duration<double>(Clock::now() - t0).count();
+        if (r.outputs[2].rows() != rows) {
+            std::fprintf(stderr, "gather rows mismatch\n");
+            return 2;
+        }
+        if (s >= warmup) timed += d;
+    }
+    const double bytes = double(rows) * cols * 4;
+    std::printf("{\"mode\": \"slicing\", \"rows\": %zu, \"cols\": %zu, \"slices\": %zu, \"steps\": %ld,"
+                " \"workers\": %zu, \"seconds\": %.6f, \"ms_per_step\": %.4f, \"gbs\": %.4f}\n",
+                rows, cols, slices, steps, workers, timed, 1e3 * timed / steps, bytes * steps / timed / 1e9);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     std::string mode = sarg(argc, argv, "--mode", "gather");
     try {
         if (mode == "gather") return run_gather(argc, argv);
         if (mode == "sgd") return run_sgd(argc, argv);
+        if (mode == "slicing") return run_slicing(argc, argv);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "ref_driver: %s\n", e.what());
         return 1;

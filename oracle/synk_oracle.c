@@ -83,6 +83,23 @@ void so_scale(int dtype, void* buf, double factor, uint64_t n) {
     for (uint64_t i = 0; i < n; ++i) st(dtype, buf, i, ld(dtype, buf, i) * factor);
 }
 
+/* Synthetic-data stream (no reference counterpart; the reference generates
+ * its bench/acceptance datasets on the host with libstdc++ RNGs,
+ * bench.cpp:41-58): value i = (splitmix64(seed + i*golden) >> 40) * 2^-23 - 1,
+ * exact in f32 and f64. Mirrors synk_fill_uniform. */
+static uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+void so_fill_uniform(int dtype, void* dst, uint64_t n, uint64_t seed, uint64_t first) {
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t k = splitmix64(seed + (first + i) * 0x9E3779B97F4A7C15ull) >> 40;
+        st(dtype, dst, i, (double)k * 0x1p-23 - 1.0);
+    }
+}
+
 /* replicated.cpp:16-29 */
 int so_tree_fold(int dtype, int op, const void* const* parts, uint64_t world, uint64_t n,
                  void* out) {

@@ -41,6 +41,10 @@ int so_weighted_mean(int dtype, void* acc, double wa, const void* other, double 
 /* tensor.cpp:367-373 — v = T(f64(v) * factor). */
 void so_scale(int dtype, void* buf, double factor, uint64_t n);
 
+/* Synthetic U[-1,1) stream used for HBM-resident bench/test datasets
+ * (mirrors synk_fill_uniform; no reference counterpart). */
+void so_fill_uniform(int dtype, void* dst, uint64_t n, uint64_t seed, uint64_t first);
+
 /* replicated.cpp:16-29 — binomial-tree fold of `world` replicas into out
  * (Mean = Sum then scale by 1/world). */
 int so_tree_fold(int dtype, int op, const void* const* parts, uint64_t world, uint64_t n, void* out);

@@ -113,6 +113,46 @@ __global__ void __launch_bounds__(kBlock) fill_kernel(T* __restrict__ a, uint64_
     for (uint64_t i = tid; i < n; i += (uint64_t)gridDim.x * kBlock) a[i] = v;
 }
 
+// Counter-based U[-1,1) synthetic data: element i of the virtual array gets
+// splitmix64(seed + i*golden) -> top 24 bits -> k * 2^-23 - 1 (exact in f32/f64).
+// Same formula as oracle/synk_oracle.c so_fill_uniform.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock) fill_uniform_kernel(T* __restrict__ a, uint64_t n, uint64_t seed,
+                                                              uint64_t first) {
+    const uint64_t stride = (uint64_t)gridDim.x * kBlock;
+    for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride) {
+        const uint64_t k = splitmix64(seed + (first + i) * 0x9E3779B97F4A7C15ull) >> 40;
+        a[i] = (T)((double)k * 0x1p-23 - 1.0);
+    }
+}
+
+template <>
+__global__ void __launch_bounds__(kBlock) fill_uniform_kernel<float>(float* __restrict__ a, uint64_t n, uint64_t seed,
+                                                                     uint64_t first) {
+    // four elements per thread per iteration, one 16-byte store when aligned
+    const uint64_t stride = (uint64_t)gridDim.x * kBlock;
+    const uint64_t nv = ((uintptr_t)a & 15) == 0 ? n / 4 : 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * kBlock + threadIdx.x; v < nv; v += stride) {
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t k = splitmix64(seed + (first + 4 * v + j) * 0x9E3779B97F4A7C15ull) >> 40;
+            r[j] = (float)k * 0x1p-23f - 1.0f;
+        }
+        reinterpret_cast<float4*>(a)[v] = make_float4(r[0], r[1], r[2], r[3]);
+    }
+    for (uint64_t i = 4 * nv + (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += stride) {
+        const uint64_t k = splitmix64(seed + (first + i) * 0x9E3779B97F4A7C15ull) >> 40;
+        a[i] = (float)k * 0x1p-23f - 1.0f;
+    }
+}
+
 // ---- ordered fold over contributions (slices / ranks) ---------------------------
 
 constexpr int kMaxParts = 64;
@@ -314,6 +354,21 @@ int synk_fill(synk_dev* d, int dtype, void* dst, double value, uint64_t n) {
     if (dtype == SYNK_F32) fill_kernel<float><<<grid, kBlock, 0, d->stream>>>((float*)dst, n, (float)value);
     else fill_kernel<double><<<grid, kBlock, 0, d->stream>>>((double*)dst, n, value);
     SYNK_LAUNCHED("fill_kernel");
+    return SYNK_OK;
+}
+
+int synk_fill_uniform(synk_dev* d, int dtype, void* dst, uint64_t n, uint64_t seed, uint64_t first) {
+    SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_fill_uniform: bad dtype");
+    if (n == 0) return SYNK_OK;
+    synk::DeviceGuard g(d->device);
+    if (dtype == SYNK_F32) {
+        unsigned grid = synk::grid_for(d, (n + 3) / 4, kBlock);
+        fill_uniform_kernel<float><<<grid, kBlock, 0, d->stream>>>((float*)dst, n, seed, first);
+    } else {
+        unsigned grid = synk::grid_for(d, n, kBlock);
+        fill_uniform_kernel<double><<<grid, kBlock, 0, d->stream>>>((double*)dst, n, seed, first);
+    }
+    SYNK_LAUNCHED("fill_uniform_kernel");
     return SYNK_OK;
 }
 

@@ -249,6 +249,25 @@ void ReplicatedVariable::scatter_value(const SharedInputArray& data, const std::
     scatter_value(data.view(), indexes);
 }
 
+void ReplicatedVariable::scatter_uniform(const std::vector<std::size_t>& shape, DType dtype, std::uint64_t seed) {
+    detail::VarRecord& rec = live(rec_, "scatter_uniform");
+    if (shape.empty()) throw ShapeError("scatter_uniform: a rank-0 shape has no rows to scatter");
+    const std::size_t row = element_count(shape) / std::max<std::size_t>(shape[0], 1);
+    std::vector<RowRange> parts = partition_rows(shape[0], rec.replicas.size());
+    detail::PoolState& st = *rec.pool;
+    detail::run_pool_phase(st, PhaseKind::ScatterVar, [&](std::size_t r) {
+        std::vector<std::size_t> s = shape;
+        s[0] = parts[r].stop - parts[r].start;
+        DevBuffer b = DevBuffer::alloc(st.ranks[r], s, dtype);
+        detail::check(synk_fill_uniform(st.handles[r], detail::synk_dtype(dtype), b.data(), b.size(), seed,
+                                        parts[r].start * row),
+                      "scatter_uniform");
+        detail::dev_sync(st.ranks[r]);
+        rec.replicas[r] = std::move(b);
+    });
+    if (rec.replicas.size() > 1) rec.coherent = false;
+}
+
 bool ReplicatedVariable::replicas_coherent() const {
     detail::VarRecord& rec = live(rec_, "replicas_coherent");
     no_phase(rec, "replicas_coherent");

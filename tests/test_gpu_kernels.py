@@ -36,6 +36,19 @@ def test_gather_bit_exact_vs_oracle(oracle):
                 assert got.tobytes() == oracle.gather_rows(src, idx).tobytes()
 
 
+def test_fill_uniform_matches_oracle_stream(oracle):
+    with Ranks(1) as R:
+        for dtype, code in ((np.float32, F32), (np.float64, F64)):
+            for n, first, off in ((1, 0, 0), (4099, 0, 0), (1000, 123457, 0), (1001, 5, 1), (1 << 20, 1 << 33, 0)):
+                d = R.alloc((n + off) * np.dtype(dtype).itemsize)
+                check(lib().synk_fill_uniform(R[0], code, _vp(d + off * np.dtype(dtype).itemsize), _u64(n), _u64(9),
+                                              _u64(first)), "fill_uniform")
+                check(R.sync(), "sync")
+                got = R.download(d, (n + off,), dtype)[off:]
+                assert got.tobytes() == oracle.fill_uniform(n, 9, first, dtype).tobytes()
+                assert got.min() >= -1 and got.max() < 1
+
+
 def test_gather_golden_vectors():
     g = golden("gather.npz")
     with Ranks(1) as R:
