@@ -8,6 +8,7 @@
 // f64 with one cast on store.
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -224,6 +225,63 @@ __global__ void __launch_bounds__(kBlock) colstats_partial_kernel(
     pmin[o] = mn;
 }
 
+// Vector variant (16-byte groups of 4 f32 / 2 f64 columns per thread): 8
+// rows in flight per thread = 128 B (volatile asm keeps all 8 loads ahead of
+// the folds), non-allocating loads. Same fold order per column as the scalar
+// kernel, so results are identical.
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock) colstats_partial_vec_kernel(
+    const T* __restrict__ x, uint64_t rows, uint64_t cols, uint64_t rows_per_chunk, uint32_t rpb,
+    double* __restrict__ psum, T* __restrict__ pmax, T* __restrict__ pmin) {
+    // rpb > 1 (narrow rows): the CTA covers rpb rows per step, thread group
+    // tr takes rows r0+tr, r0+tr+rpb, ... and owns partial slot chunk*rpb+tr.
+    using V = typename Vec16<T>::V;
+    constexpr int N = Vec16<T>::N;
+    const uint64_t ncv = cols / N;
+    const uint64_t cv = rpb > 1 ? threadIdx.x % ncv : (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+    const uint32_t tr = rpb > 1 ? threadIdx.x / (uint32_t)ncv : 0;
+    const uint64_t r0 = (uint64_t)blockIdx.y * rows_per_chunk + tr;
+    const uint64_t r1 = r0 - tr + rows_per_chunk < rows ? r0 - tr + rows_per_chunk : rows;
+    if (cv >= ncv || tr >= rpb) return;
+    const V* xv = reinterpret_cast<const V*>(x) + cv;
+    double s[N];
+    T mx[N], mn[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) s[j] = 0.0, mx[j] = -INFINITY, mn[j] = INFINITY;
+    auto fold = [&](V vv) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const T e = lane<T>(vv, j);
+            s[j] += (double)e;
+            mx[j] = e > mx[j] ? e : mx[j];
+            mn[j] = e < mn[j] ? e : mn[j];
+        }
+    };
+    uint64_t r = r0;
+    for (; r + 7 * (uint64_t)rpb < r1; r += 8 * (uint64_t)rpb) {
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = ld_stream16(xv + (r + k * (uint64_t)rpb) * ncv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fold(*reinterpret_cast<V*>(&v[k]));
+    }
+    for (; r < r1; r += rpb) {
+        uint4 v = ld_stream16(xv + r * ncv);
+        fold(*reinterpret_cast<V*>(&v));
+    }
+    const uint64_t o = ((uint64_t)blockIdx.y * rpb + tr) * cols + cv * N;
+#pragma unroll
+    for (int j = 0; j < N; ++j) psum[o + j] = s[j], pmax[o + j] = mx[j], pmin[o + j] = mn[j];
+}
+
 template <class T>
 __global__ void __launch_bounds__(kBlock) colstats_final_kernel(
     uint64_t chunks, uint64_t cols, const double* __restrict__ psum, const T* __restrict__ pmax,
@@ -245,27 +303,39 @@ __global__ void __launch_bounds__(kBlock) colstats_final_kernel(
 
 template <class T>
 int column_stats_t(synk_dev* d, const T* x, uint64_t rows, uint64_t cols, T* so, T* mxo, T* mno) {
-    uint64_t col_tiles = (cols + kBlock - 1) / kBlock;
-    // Enough row chunks for ~4 CTAs per SM, each chunk >= 64 rows.
+    constexpr int N = Vec16<T>::N;
+    static const bool force_scalar = getenv("SYNK_COLSTATS_SCALAR") != nullptr;  // diagnostics
+    const bool vec = !force_scalar && cols % N == 0 && ((uintptr_t)x & 15) == 0;
+    const uint64_t threads_per_row = vec ? cols / N : cols;
+    // Narrow rows (vector path): one CTA step covers rpb whole rows.
+    const uint32_t rpb = vec && threads_per_row < kBlock ? (uint32_t)(kBlock / threads_per_row) : 1;
+    const uint64_t col_tiles = rpb > 1 ? 1 : (threads_per_row + kBlock - 1) / kBlock;
+    // Enough row chunks for ~4 CTAs per SM, each chunk >= 64 rows per row group.
     uint64_t want = ((uint64_t)d->num_sms * 4 + col_tiles - 1) / col_tiles;
-    uint64_t chunks = rows / 64;
+    uint64_t chunks = rows / (64 * rpb);
     if (chunks > want) chunks = want;
     if (chunks > 65535) chunks = 65535;
     if (chunks < 1) chunks = 1;
     uint64_t per = (rows + chunks - 1) / chunks;
     if (per == 0) per = 1;
     chunks = rows == 0 ? 1 : (rows + per - 1) / per;
-    size_t bytes = chunks * cols * (sizeof(double) + 2 * sizeof(T));
+    const uint64_t slots = chunks * rpb;
+    size_t bytes = slots * cols * (sizeof(double) + 2 * sizeof(T));
     void* ws = nullptr;
     SYNK_CU(cudaMallocAsync(&ws, bytes, d->stream));
     double* psum = (double*)ws;
-    T* pmax = (T*)(psum + chunks * cols);
-    T* pmin = pmax + chunks * cols;
+    T* pmax = (T*)(psum + slots * cols);
+    T* pmin = pmax + slots * cols;
     dim3 grid((unsigned)col_tiles, (unsigned)chunks);
-    colstats_partial_kernel<T><<<grid, kBlock, 0, d->stream>>>(x, rows, cols, per, psum, pmax, pmin);
-    SYNK_LAUNCHED("colstats_partial_kernel");
-    colstats_final_kernel<T><<<(unsigned)col_tiles, kBlock, 0, d->stream>>>(chunks, cols, psum, pmax,
-                                                                            pmin, so, mxo, mno);
+    if (vec) {
+        colstats_partial_vec_kernel<T><<<grid, kBlock, 0, d->stream>>>(x, rows, cols, per, rpb, psum, pmax, pmin);
+        SYNK_LAUNCHED("colstats_partial_vec_kernel");
+    } else {
+        colstats_partial_kernel<T><<<grid, kBlock, 0, d->stream>>>(x, rows, cols, per, psum, pmax, pmin);
+        SYNK_LAUNCHED("colstats_partial_kernel");
+    }
+    colstats_final_kernel<T><<<(unsigned)((cols + kBlock - 1) / kBlock), kBlock, 0, d->stream>>>(
+        slots, cols, psum, pmax, pmin, so, mxo, mno);
     SYNK_LAUNCHED("colstats_final_kernel");
     SYNK_CU(cudaFreeAsync(ws, d->stream));
     return SYNK_OK;
