@@ -59,6 +59,7 @@ def parse():
     p.add_argument("--c3-rows", type=int, default=8_388_608)
     p.add_argument("--c3-cols", type=int, default=1024)
     p.add_argument("--c3-slices", type=int, default=4)
+    p.add_argument("--no-c4", action="store_true", help="skip the C4 shared-variable sync sweep")
     p.add_argument("--dry-run", action="store_true",
                    help="exercise only the launch/rank coordination (no GPU work); used by CPU tests")
     return p.parse_args()
@@ -261,6 +262,58 @@ def slicing_c3(sk, pool, args, n_gpus, peak, peak_kind):
     return out
 
 
+def collectives_c4(sk, args, n_gpus):
+    """C4: Replicated.all_reduce("mean") and broadcast(0) of f32 buffers from
+    1 KiB to 1 GiB, timed per call on the host (phase protocol + peer-memory
+    kernel + stream sync). busbw = S/t * 2(W-1)/W (all-reduce), S/t (broadcast).
+    With one GPU the W=2 ranks share it, so the peer-memory kernels move the
+    bytes through local HBM instead of NVLink (stated in the output)."""
+    world = n_gpus if n_gpus >= 2 else 2
+    devices = list(range(n_gpus)) if n_gpus >= 2 else [0, 0]
+    sizes = [1 << k for k in range(10, 31, 3)] + [1 << 30]
+    rng = np.random.default_rng(1000)
+    sweep = []
+    with sk.Pool(workers=world, devices=devices) as pool:
+        for S in sizes:
+            n = S // 4
+            var = sk.replicate(pool, np.zeros(n, np.float32))
+            for r in range(world):
+                var.set(r, rng.uniform(-1, 1, n).astype(np.float32))
+            reps = 200 if S <= (1 << 20) else (30 if S <= (1 << 27) else 8)
+            for _ in range(3):
+                var.all_reduce("mean")
+                var.broadcast(0)
+            t = time.perf_counter()
+            for _ in range(reps):
+                var.all_reduce("mean")
+            t_ar = (time.perf_counter() - t) / reps
+            t = time.perf_counter()
+            for _ in range(reps):
+                var.broadcast(0)
+            t_bc = (time.perf_counter() - t) / reps
+            coherent = var.coherent
+            del var
+            sweep.append({"bytes": S, "allreduce_us": 1e6 * t_ar, "allreduce_busbw_gbs": S / t_ar * 2 * (world - 1) / world / 1e9,
+                          "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9, "coherent": coherent})
+    out = {"config": "C4: all_reduce mean + broadcast(0) of f32 buffers 1 KiB - 1 GiB, W=%d ranks" % world,
+           "ranks": world, "devices": devices,
+           "link": "NVLink peer memory" if n_gpus >= 2 else "1 GPU: both ranks share it, peer-memory kernels run "
+                                                             "over local HBM (NVLink unmeasured)",
+           "sweep": sweep}
+    if not args.no_cpu_baseline:
+        ref = []
+        for S in (1 << 10, 1 << 16, 1 << 20, 1 << 26):
+            res, err = run_reference_driver("collective", ["--bytes", S, "--workers", world, "--steps", 3,
+                                                           "--warmup", 1])
+            if res is None:
+                ref = {"unavailable": err}
+                break
+            ref.append({k: res[k] for k in ("bytes", "allreduce_us", "allreduce_busbw_gbs", "broadcast_us",
+                                            "broadcast_busbw_gbs")})
+        out["cpu_baseline"] = {"kind": "reference", "cores": world, "sweep": ref}
+    return out
+
+
 def ours(args, n_gpus):
     import paper_1710_04162_b200 as sk
 
@@ -445,6 +498,10 @@ def ours(args, n_gpus):
         c3 = slicing_c3(sk, pool, args, n_gpus, peak, peak_kind)
 
     pool.shutdown()
+    # ---- shared-variable sync sweep (C4): its own pool (one live pool per process) ----
+    c4 = None
+    if not args.no_c4:
+        c4 = collectives_c4(sk, args, n_gpus)
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * region_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -464,6 +521,8 @@ def ours(args, n_gpus):
         line["sync_sgd_wide_bf16"] = sgd5
     if c3:
         line["slicing_c3"] = c3
+    if c4:
+        line["collectives_c4"] = c4
     return line
 
 

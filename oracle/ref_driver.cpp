@@ -9,6 +9,8 @@
 //           gather_rows.
 //   sgd:    SyncSgd::train_step of the MLP (in-width-out, layers 2) on a
 //           SharedInputArray dataset, indexed batches (C1).
+//   collective: ReplicatedVariable::all_reduce(Mean) and broadcast(0) of a
+//           `--bytes` f32 buffer at `--workers` ranks (C4).
 //   slicing: ParallelFunction over an explicit scatter input [rows x cols]
 //           f32 with num_slices slices; the kernel returns column sums (Sum),
 //           column maxima (Max) and the shard itself (Gather) -- the
@@ -214,12 +216,48 @@ static int run_slicing(int argc, char** argv) {
     return 0;
 }
 
+static int run_collective(int argc, char** argv) {
+    const std::size_t bytes = arg(argc, argv, "--bytes", 1 << 20);
+    const long steps = arg(argc, argv, "--steps", 5), warmup = arg(argc, argv, "--warmup", 1);
+    const std::size_t workers = std::max(2L, arg(argc, argv, "--workers", 2));
+    const std::size_t n = std::max<std::size_t>(1, bytes / 4);
+    WorkerPool pool = WorkerPool::fork(ForkOptions{.workers = workers, .pin_threads = true});
+    ReplicatedVariable var = replicate(pool, NdBuffer::zeros({n}, DType::Float32));
+    std::uint64_t seed = 1000;
+    for (std::size_t r = 0; r < workers; ++r) {
+        NdBuffer v = NdBuffer::zeros({n}, DType::Float32);
+        for (float& e : v.as_mut<float>()) e = float(double(splitmix(seed) >> 11) * (2.0 / 9007199254740992.0) - 1.0);
+        var.set_value(r, v);
+    }
+    double t_ar = 0.0, t_bc = 0.0;
+    for (long s = 0; s < warmup + steps; ++s) {
+        auto t0 = Clock::now();
+        var.all_reduce(ReduceOp::Mean);
+        auto t1 = Clock::now();
+        var.broadcast(0);
+        auto t2 = Clock::now();
+        if (s >= warmup) {
+            t_ar += std::chrono::duration<double>(t1 - t0).count();
+            t_bc += std::chrono::duration<double>(t2 - t1).count();
+        }
+    }
+    const double S = double(n) * 4, W = double(workers);
+    t_ar /= double(steps);
+    t_bc /= double(steps);
+    std::printf("{\"mode\": \"collective\", \"bytes\": %.0f, \"workers\": %zu, \"steps\": %ld,"
+                " \"allreduce_us\": %.3f, \"allreduce_busbw_gbs\": %.4f, \"broadcast_us\": %.3f,"
+                " \"broadcast_busbw_gbs\": %.4f}\n",
+                S, workers, steps, 1e6 * t_ar, S / t_ar * 2 * (W - 1) / W / 1e9, 1e6 * t_bc, S / t_bc / 1e9);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     std::string mode = sarg(argc, argv, "--mode", "gather");
     try {
         if (mode == "gather") return run_gather(argc, argv);
         if (mode == "sgd") return run_sgd(argc, argv);
         if (mode == "slicing") return run_slicing(argc, argv);
+        if (mode == "collective") return run_collective(argc, argv);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "ref_driver: %s\n", e.what());
         return 1;

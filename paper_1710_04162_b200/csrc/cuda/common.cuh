@@ -15,8 +15,13 @@ struct synk_dev {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
-    int* flags_dev = nullptr;   // [0] bounds error, [1] scratch result
+    int* flags_dev = nullptr;   // [1] scratch result of synchronous checks
     int* flags_host = nullptr;  // pinned mirror for synchronous checks
+    // Sticky device-detected error flag (gather bounds), in mapped pinned host
+    // memory: kernels write it only on error, synk_sync reads it after the
+    // stream drains -- no extra copy on the phase-exit path.
+    volatile int* err_host = nullptr;
+    int* err_dev = nullptr;
     std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
     int marks_used = 0;
 };

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kBlock) gather_rows_kernel(
         if (lane < kRows && r0 + lane < n_idx) {
             mine = idx[r0 + lane];
             ok = mine < src_rows;
-            if (!ok) atomicExch(err, 1);
+            if (!ok) *(volatile int*)err = 1;  // mapped host flag: plain store, every writer stores 1
         }
         uint64_t row[kRows];
         int valid[kRows];
@@ -108,7 +108,7 @@ int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     gather_rows_kernel<BYTES><<<(unsigned)blocks, kBlock, 0, d->stream>>>(
-        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, (V*)dst, d->flags_dev);
+        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, (V*)dst, d->err_dev);
     SYNK_LAUNCHED("gather_rows_kernel");
     return SYNK_OK;
 }

@@ -25,11 +25,13 @@ constexpr int BM = 64, BN = 64, BK = 16, kThreads = 256;
 enum Epi { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_TANH = 2, EPI_TANH_GRAD = 3 };
 
 // C[m,n] = epi( sum_k A(m,k) B(k,n) ), A(m,k) = A[m*am + k*ak], B(k,n) = B[k*bk + n*bn]
+// Split-K (gridDim.z > 1): CTA z sums k in [z*kper, (z+1)*kper) and stores the
+// raw partial to C + z*M*N (ldc = N); splitk_reduce_kernel folds the partials.
 template <class T>
 __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
     int epi, int64_t M, int64_t N, int64_t K, const T* __restrict__ A, int64_t am, int64_t ak,
     const T* __restrict__ B, int64_t bk, int64_t bn, T* __restrict__ C, int64_t ldc,
-    const T* __restrict__ bias, const T* __restrict__ act) {
+    const T* __restrict__ bias, const T* __restrict__ act, int64_t kper) {
     __shared__ T As[BK][BM + 1];
     __shared__ T Bs[BK][BN + 1];
     const int tid = threadIdx.x;
@@ -41,7 +43,13 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
 
-    for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    const int64_t kbeg = (int64_t)blockIdx.z * kper;
+    const int64_t kend = kbeg + kper < K ? kbeg + kper : K;
+    if (gridDim.z > 1) {
+        C += (int64_t)blockIdx.z * M * N;
+        epi = -1;  // raw partial
+    }
+    for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             int idx = tid + i * kThreads;
@@ -49,13 +57,13 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
             if (ak == 1) { kk = idx % BK; mm = idx / BK; }   // K contiguous in memory
             else { mm = idx % BM; kk = idx / BM; }
             int64_t gm = m0 + mm, gk = k0 + kk;
-            As[kk][mm] = (gm < M && gk < K) ? A[gm * am + gk * ak] : T(0);
+            As[kk][mm] = (gm < M && gk < kend) ? A[gm * am + gk * ak] : T(0);
             int nn;
             if (bn == 1) { nn = idx % BN; kk = idx / BN; }   // N contiguous in memory
             else { kk = idx % BK; nn = idx / BK; }
             int64_t gn = n0 + nn;
             gk = k0 + kk;
-            Bs[kk][nn] = (gn < N && gk < K) ? B[gk * bk + gn * bn] : T(0);
+            Bs[kk][nn] = (gn < N && gk < kend) ? B[gk * bk + gn * bn] : T(0);
         }
         __syncthreads();
 #pragma unroll
@@ -92,15 +100,86 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
     }
 }
 
+// Fixed (device-independent, so results do not depend on the SM count) split
+// of K for f32 products with too few output tiles to fill the GPU: ~2 CTAs per
+// SM of a 148-SM B200, at least 32 k per split. f64 stays unsplit (its
+// trajectories are held to 1e-10 against the reference's sequential sums).
+constexpr int64_t kSplitTargetCtas = 296;
+
+inline int64_t split_k(int es, int64_t M, int64_t N, int64_t K, int64_t* kper) {
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    int64_t s = 1;
+    if (es == 4 && tiles * 2 < kSplitTargetCtas) {
+        s = kSplitTargetCtas / tiles;
+        if (s > K / 32) s = K / 32;
+        if (s > 32) s = 32;
+        if (s < 1) s = 1;
+    }
+    int64_t per = (K + s - 1) / s;
+    per = (per + BK - 1) / BK * BK;
+    if (per < BK) per = BK;
+    *kper = per;
+    return K == 0 ? 1 : (K + per - 1) / per;
+}
+
+// C = epi(sum_z P[z]) in fixed z order (f64 accumulation of the f32 partials).
+template <class T>
+__global__ void __launch_bounds__(kThreads) splitk_reduce_kernel(
+    int epi, int64_t S, int64_t M, int64_t N, const T* __restrict__ P, T* __restrict__ C, int64_t ldc,
+    const T* __restrict__ bias, const T* __restrict__ act) {
+    const int64_t total = M * N;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += (int64_t)gridDim.x * kThreads) {
+        double acc = 0.0;
+        for (int64_t z = 0; z < S; ++z) acc += (double)P[z * total + i];
+        const int64_t gm = i / N, gn = i % N;
+        T v = (T)acc;
+        if (epi == EPI_BIAS) v = v + bias[gn];
+        else if (epi == EPI_BIAS_TANH) v = tanh(v + bias[gn]);
+        else if (epi == EPI_TANH_GRAD) {
+            T a = act[gm * ldc + gn];
+            v = v * (T(1) - a * a);
+        }
+        C[gm * ldc + gn] = v;
+    }
+}
+
 template <class T>
 int gemm(synk_dev* d, int epi, int64_t M, int64_t N, int64_t K, const T* A, int64_t am, int64_t ak,
-         const T* B, int64_t bk, int64_t bn, T* C, int64_t ldc, const T* bias, const T* act) {
+         const T* B, int64_t bk, int64_t bn, T* C, int64_t ldc, const T* bias, const T* act, T* partials) {
     if (M == 0 || N == 0) return SYNK_OK;
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-    gemm_simt_kernel<T><<<grid, kThreads, 0, d->stream>>>(epi, M, N, K, A, am, ak, B, bk, bn, C, ldc,
-                                                          bias, act);
+    int64_t kper = 0;
+    const int64_t S = split_k(sizeof(T), M, N, K, &kper);
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)S);
+    if (S == 1) {
+        gemm_simt_kernel<T><<<grid, kThreads, 0, d->stream>>>(epi, M, N, K, A, am, ak, B, bk, bn, C, ldc, bias,
+                                                              act, K > 0 ? K : 1);
+        SYNK_LAUNCHED("gemm_simt_kernel");
+        return SYNK_OK;
+    }
+    SYNK_REQUIRE(partials != nullptr, SYNK_EARG, "mlp gemm: split-K needs a partials workspace");
+    gemm_simt_kernel<T><<<grid, kThreads, 0, d->stream>>>(epi, M, N, K, A, am, ak, B, bk, bn, partials, N,
+                                                          nullptr, nullptr, kper);
     SYNK_LAUNCHED("gemm_simt_kernel");
+    unsigned rgrid = (unsigned)std::min<int64_t>((M * N + kThreads - 1) / kThreads, 148 * 4);
+    splitk_reduce_kernel<T><<<rgrid, kThreads, 0, d->stream>>>(epi, S, M, N, partials, C, ldc, bias, act);
+    SYNK_LAUNCHED("splitk_reduce_kernel");
     return SYNK_OK;
+}
+
+// Largest split-K partial buffer (elements) over the products of one loss/grad pass.
+uint64_t splitk_elems(int es, const uint64_t* dims, uint32_t layers, uint64_t n) {
+    uint64_t best = 0;
+    auto see = [&](int64_t M, int64_t N, int64_t K) {
+        int64_t kper;
+        int64_t S = split_k(es, M, N, K, &kper);
+        if (S > 1 && (uint64_t)(S * M * N) > best) best = (uint64_t)(S * M * N);
+    };
+    for (uint32_t l = 0; l < layers; ++l) {
+        see((int64_t)n, (int64_t)dims[l + 1], (int64_t)dims[l]);
+        see((int64_t)dims[l], (int64_t)dims[l + 1], (int64_t)n);
+        if (l > 0) see((int64_t)n, (int64_t)dims[l], (int64_t)dims[l + 1]);
+    }
+    return best;
 }
 
 // delta = (pred - y) * inv_n ; per-CTA partial of sum (pred - y)^2 in f64.
@@ -158,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) bias_grad_kernel(const T* __restrict
 
 struct Plan {
     uint64_t woff[64], boff[64];
-    uint64_t total = 0, maxd = 0, act_elems = 0;
+    uint64_t total = 0, maxd = 0, act_elems = 0, splitk = 0;
 };
 
 int make_plan(const uint64_t* dims, uint32_t layers, uint64_t n, Plan* p) {
@@ -176,16 +255,18 @@ int make_plan(const uint64_t* dims, uint32_t layers, uint64_t n, Plan* p) {
     }
     for (uint32_t l = 0; l <= layers; ++l) p->maxd = dims[l] > p->maxd ? dims[l] : p->maxd;
     p->total = at;
+    p->splitk = splitk_elems(4, dims, layers, n);  // f32 only; f64 products are not split
     return SYNK_OK;
 }
 
 constexpr int kLossBlocks = 128;
 
+// workspace: acts[1..L] | delta ping | delta pong | loss partials | split-K partials
 uint64_t ws_bytes(int dtype, const Plan& p, uint64_t n) {
     uint64_t es = synk::dtype_bytes(dtype);
     uint64_t bytes = (p.act_elems + 2 * n * p.maxd) * es;
     bytes = (bytes + 255) / 256 * 256;
-    return bytes + kLossBlocks * sizeof(double);
+    return bytes + kLossBlocks * sizeof(double) + (es == 4 ? p.splitk * es : 0);
 }
 
 template <class T>
@@ -205,12 +286,13 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     uint64_t es = sizeof(T);
     uint64_t off = ((P.act_elems + 2 * n * P.maxd) * es + 255) / 256 * 256;
     double* partial = (double*)((char*)ws + off);
+    T* skp = (T*)(partial + kLossBlocks);
 
     for (uint32_t l = 0; l < layers; ++l) {
         int64_t din = dims[l], dout = dims[l + 1];
         int epi = (l + 1 < layers) ? EPI_BIAS_TANH : EPI_BIAS;
         if (int rc = gemm<T>(d, epi, n, dout, din, acts[l], din, 1, theta + P.woff[l], dout, 1,
-                             acts[l + 1], dout, theta + P.boff[l], nullptr);
+                             acts[l + 1], dout, theta + P.boff[l], nullptr, skp);
             rc != SYNK_OK)
             return rc;
     }
@@ -231,7 +313,7 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
         int64_t din = dims[l], dout = dims[l + 1];
         // gW = a_l^T delta : M=din, N=dout, K=n
         if (int rc = gemm<T>(d, EPI_STORE, din, dout, n, acts[l], 1, din, delta, dout, 1,
-                             grad + P.woff[l], dout, nullptr, nullptr);
+                             grad + P.woff[l], dout, nullptr, nullptr, skp);
             rc != SYNK_OK)
             return rc;
         bias_grad_kernel<T><<<(unsigned)((dout + 31) / 32), kThreads, 0, d->stream>>>(
@@ -240,7 +322,7 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
         if (l > 0) {
             // delta_prev = (delta W^T) * (1 - a_l^2) : M=n, N=din, K=dout
             if (int rc = gemm<T>(d, EPI_TANH_GRAD, n, din, dout, delta, dout, 1, theta + P.woff[l], 1,
-                                 dout, spare, din, nullptr, acts[l]);
+                                 dout, spare, din, nullptr, acts[l], skp);
                 rc != SYNK_OK)
                 return rc;
             T* t = delta;

@@ -10,6 +10,8 @@
 #include <mutex>
 #include <set>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace synk {
@@ -100,6 +102,11 @@ int synk_open(int world, const int* device_ids, synk_dev** out) {
         SYNK_CU(cudaMalloc(&d->flags_dev, 4 * sizeof(int)));
         SYNK_CU(cudaMemset(d->flags_dev, 0, 4 * sizeof(int)));
         SYNK_CU(cudaHostAlloc(&d->flags_host, 4 * sizeof(int), cudaHostAllocPortable));
+        void* eh = nullptr;
+        SYNK_CU(cudaHostAlloc(&eh, 64, cudaHostAllocPortable | cudaHostAllocMapped));
+        std::memset(eh, 0, 64);
+        d->err_host = static_cast<volatile int*>(eh);
+        SYNK_CU(cudaHostGetDevicePointer((void**)&d->err_dev, eh, 0));
         out[r] = d;
     }
     cudaSetDevice(prev);
@@ -113,6 +120,7 @@ int synk_close(synk_dev* d) {
     cudaStreamDestroy(d->stream);
     cudaFree(d->flags_dev);
     cudaFreeHost(d->flags_host);
+    cudaFreeHost(const_cast<int*>(d->err_host));
     for (cudaEvent_t e : d->marks) cudaEventDestroy(e);
     delete d;
     return SYNK_OK;
@@ -129,12 +137,9 @@ int synk_bind(const synk_dev* d) {
 
 int synk_sync(synk_dev* d) {
     DeviceGuard g(d->device);
-    SYNK_CU(cudaMemcpyAsync(d->flags_host, d->flags_dev, sizeof(int), cudaMemcpyDeviceToHost,
-                            d->stream));
     SYNK_CU(cudaStreamSynchronize(d->stream));
-    if (d->flags_host[0] != 0) {
-        cudaMemsetAsync(d->flags_dev, 0, sizeof(int), d->stream);
-        cudaStreamSynchronize(d->stream);
+    if (d->err_host[0] != 0) {
+        d->err_host[0] = 0;
         return fail(SYNK_EBOUNDS, "gather_rows(): index out of range (device check)");
     }
     return SYNK_OK;

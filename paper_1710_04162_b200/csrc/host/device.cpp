@@ -27,6 +27,7 @@ void check(int rc, const char* what) {
 }
 
 RankDevice::~RankDevice() {
+    if (staging) synk_host_free(staging);
     if (h && scratch) synk_free(h, scratch);
     if (h) synk_close(h);
 }
@@ -63,7 +64,17 @@ void dev_to_host_into(const DevBuffer& buf, std::byte* dst) {
 
 NdBuffer dev_to_host(const DevBuffer& buf) {
     NdBuffer out = NdBuffer::uninitialized(buf.shape(), buf.dtype());
-    if (buf.byte_size()) {
+    const std::size_t bytes = buf.byte_size();
+    if (bytes && bytes <= RankDevice::kStagingBytes) {
+        RankDevice& rd = *buf.owner();
+        std::lock_guard<std::mutex> lock(rd.staging_mu);
+        if (!rd.staging) check(synk_host_alloc(RankDevice::kStagingBytes, &rd.staging), "staging alloc");
+        check(synk_copy(rd.h, rd.staging, buf.data(), bytes), "D2H copy");
+        dev_sync(buf.owner());
+        std::memcpy(out.bytes_mut(), rd.staging, bytes);
+        return out;
+    }
+    if (bytes) {
         dev_to_host_into(buf, out.bytes_mut());
         dev_sync(buf.owner());
     }
