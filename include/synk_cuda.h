@@ -206,6 +206,11 @@ int synk_all_reduce_step(synk_dev* dev, int world, int dtype, int grad_op, int r
 int synk_gemm_prep(synk_dev* dev, int in_dtype, const void* in, uint64_t rows, uint64_t cols, uint64_t ld_in,
                    int transpose, int mode, void* out_hi, float* out_lo, uint64_t out_rows, uint64_t out_cols,
                    uint64_t ld_out);
+/* Fused bf16 staging: out = bf16(in) (rows x cols, ld_out) and out_t =
+ * bf16(in)^T (cols x rows, ld_out_t) from one read of the f32 input; either
+ * output may be NULL. */
+int synk_gemm_prep2_bf16(synk_dev* dev, const float* in, uint64_t rows, uint64_t cols, uint64_t ld_in, void* out,
+                         uint64_t ld_out, void* out_t, uint64_t ld_out_t);
 /* C[M x N] = epilogue(A[M x K] . B[N x K]^T); A, B K-major with leading dims
  * lda/ldb (16-byte aligned rows). C (row-major, ldc) and/or C^T (ldct) may be
  * NULL; out_dtype SYNK_F32 or SYNK_BF16 (act has the same dtype as C). */

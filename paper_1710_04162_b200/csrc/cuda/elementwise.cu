@@ -282,19 +282,50 @@ __global__ void __launch_bounds__(kBlock) colstats_partial_vec_kernel(
     for (int j = 0; j < N; ++j) psum[o + j] = s[j], pmax[o + j] = mx[j], pmin[o + j] = mn[j];
 }
 
+// CTA = 32 columns x 8 slot groups: group g folds slots g, g+8, ... (4 loads in
+// flight), then group 0 folds the 8 group results in order -- a fixed tree, so
+// the result is deterministic and independent of timing.
 template <class T>
 __global__ void __launch_bounds__(kBlock) colstats_final_kernel(
     uint64_t chunks, uint64_t cols, const double* __restrict__ psum, const T* __restrict__ pmax,
     const T* __restrict__ pmin, T* sum_out, T* max_out, T* min_out) {
-    uint64_t c = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (c >= cols) return;
+    __shared__ double ss[8][33];
+    __shared__ T smx[8][33], smn[8][33];
+    const int cx = threadIdx.x % 32, g = threadIdx.x / 32;
+    const uint64_t c = (uint64_t)blockIdx.x * 32 + cx;
     double s = 0.0;
     T mx = -INFINITY, mn = INFINITY;
-    for (uint64_t k = 0; k < chunks; ++k) {
-        s += psum[k * cols + c];
-        T a = pmax[k * cols + c], b = pmin[k * cols + c];
-        mx = a > mx ? a : mx;
-        mn = b < mn ? b : mn;
+    if (c < cols) {
+        uint64_t k = g;
+        for (; k + 24 < chunks; k += 32) {
+            double p[4];
+            T a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t o = (k + 8 * u) * cols + c;
+                p[u] = psum[o], a[u] = pmax[o], b[u] = pmin[o];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s += p[u];
+                mx = a[u] > mx ? a[u] : mx;
+                mn = b[u] < mn ? b[u] : mn;
+            }
+        }
+        for (; k < chunks; k += 8) {
+            s += psum[k * cols + c];
+            T a = pmax[k * cols + c], b = pmin[k * cols + c];
+            mx = a > mx ? a : mx;
+            mn = b < mn ? b : mn;
+        }
+    }
+    ss[g][cx] = s, smx[g][cx] = mx, smn[g][cx] = mn;
+    __syncthreads();
+    if (g != 0 || c >= cols) return;
+    for (int k = 1; k < 8; ++k) {
+        s += ss[k][cx];
+        mx = smx[k][cx] > mx ? smx[k][cx] : mx;
+        mn = smn[k][cx] < mn ? smn[k][cx] : mn;
     }
     if (sum_out) sum_out[c] = (T)s;
     if (max_out) max_out[c] = mx;
@@ -310,9 +341,9 @@ int column_stats_t(synk_dev* d, const T* x, uint64_t rows, uint64_t cols, T* so,
     // Narrow rows (vector path): one CTA step covers rpb whole rows.
     const uint32_t rpb = vec && threads_per_row < kBlock ? (uint32_t)(kBlock / threads_per_row) : 1;
     const uint64_t col_tiles = rpb > 1 ? 1 : (threads_per_row + kBlock - 1) / kBlock;
-    // Enough row chunks for ~4 CTAs per SM, each chunk >= 64 rows per row group.
+    // Enough row chunks for ~4 CTAs per SM, each chunk >= 16 rows per row group.
     uint64_t want = ((uint64_t)d->num_sms * 4 + col_tiles - 1) / col_tiles;
-    uint64_t chunks = rows / (64 * rpb);
+    uint64_t chunks = rows / (16 * rpb);
     if (chunks > want) chunks = want;
     if (chunks > 65535) chunks = 65535;
     if (chunks < 1) chunks = 1;
@@ -334,7 +365,7 @@ int column_stats_t(synk_dev* d, const T* x, uint64_t rows, uint64_t cols, T* so,
         colstats_partial_kernel<T><<<grid, kBlock, 0, d->stream>>>(x, rows, cols, per, psum, pmax, pmin);
         SYNK_LAUNCHED("colstats_partial_kernel");
     }
-    colstats_final_kernel<T><<<(unsigned)((cols + kBlock - 1) / kBlock), kBlock, 0, d->stream>>>(
+    colstats_final_kernel<T><<<(unsigned)((cols + 31) / 32), kBlock, 0, d->stream>>>(
         slots, cols, psum, pmax, pmin, so, mxo, mno);
     SYNK_LAUNCHED("colstats_final_kernel");
     SYNK_CU(cudaFreeAsync(ws, d->stream));

@@ -159,13 +159,27 @@ __device__ __forceinline__ void store_out(void* base, uint64_t off, float v, int
 }
 
 __device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
-                                          const uint32_t (&r)[16], bool vec_c, bool vec_act);
+                                          const uint32_t (&r)[16], bool vec_c, bool vec_act, bool have_pre, uint4 pre0, uint4 pre1);
+
+// Activation prefetch for the tanh-derivative epilogue (bf16 act, aligned
+// rows): the chunk's 32 bytes are loaded one chunk ahead so the HBM latency
+// overlaps the previous chunk's math and stores.
+struct ActPrefetch {
+    bool on;
+    const __nv_bfloat16* row;  // act row m
+    uint4 buf[2];
+    __device__ __forceinline__ void load(uint64_t nb) {
+        const uint4* src = reinterpret_cast<const uint4*>(row + nb);
+        buf[0] = src[0];
+        buf[1] = src[1];
+    }
+};
 
 template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
 __global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
-                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
+                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -177,8 +191,12 @@ __global__ void __launch_bounds__(NT, 2)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     constexpr int kBK = 128 / (KIND == 0 ? 2 : 4);  // elements per 128-byte K block
-    const int num_kb = (int)((K + kBK - 1) / kBK);
+    // split-K (gridDim.z > 1): CTA z owns K blocks [kb0, kb0 + num_kb) and
+    // stores its raw fp32 partial to plane z of C (host folds the planes).
+    const int kb0 = (int)(blockIdx.z * kb_per);
+    const int num_kb = min((int)kb_per, (int)((K + kBK - 1) / kBK) - kb0);
     const int total = passes * num_kb;
+    if (gridDim.z > 1) epi.c = static_cast<float*>(epi.c) + (uint64_t)blockIdx.z * M * epi.ldc;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -215,8 +233,8 @@ __global__ void __launch_bounds__(NT, 2)
             const CUtensorMap* mb = pass == 1 ? &b1 : &b0;
             const uint32_t full = smem_u32(&bars[s]);
             mbar_expect_tx(full, 2 * kTileBytes);
-            tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, kb * kBK, (int)m0);
-            tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, kb * kBK, (int)n0);
+            tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, (kb0 + kb) * kBK, (int)m0);
+            tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, (kb0 + kb) * kBK, (int)n0);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
@@ -254,12 +272,18 @@ __global__ void __launch_bounds__(NT, 2)
     const bool vec_c = epi.c && ((epi.ldc * es) % 16 == 0) && ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
     const bool vec_act = epi.mode == EPI_TANH_GRAD && ((epi.ldact * es) % 16 == 0) &&
                          ((reinterpret_cast<uintptr_t>(epi.act) & 15) == 0);
+    ActPrefetch pf{epi.mode == EPI_TANH_GRAD && epi.out_bf16 && vec_act && m < M,
+                   static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact, {}};
+    if (pf.on && n0 + grp * kCols + 16 <= N) pf.load(n0 + grp * kCols);
 #pragma unroll 1
     for (int c0 = grp * kCols; c0 < (grp + 1) * kCols; c0 += 16) {
+        const uint4 cur0 = pf.buf[0], cur1 = pf.buf[1];
+        const bool have = pf.on && n0 + c0 + 16 <= N;
+        if (pf.on && c0 + 16 < (grp + 1) * kCols && n0 + c0 + 32 <= N) pf.load(n0 + c0 + 16);
         uint32_t r[16];
         tmem_ld16(lane_base + c0, r);
         if (m >= M) continue;
-        epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act);
+        epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act, have, cur0, cur1);
     }
     tc_fence_before();
     __syncthreads();
@@ -272,8 +296,8 @@ __global__ void __launch_bounds__(NT, 2)
 // values r (fp32 bits): bias / tanh / tanh-derivative, then row-major C
 // (16-byte vector stores when aligned) and/or C^T (lanes = consecutive rows,
 // so each scalar store instruction is one coalesced warp segment).
-__device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
-                                          const uint32_t (&r)[16], bool vec_c, bool vec_act) {
+__device__ __forceinline__ void epi_chunk_generic(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
+                                               const uint32_t (&r)[16], bool vec_c, bool vec_act) {
     {
         float v[16];
         float act[16];
@@ -339,6 +363,137 @@ __device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64
                 if (nb + j < N) store_out(epi.ct, (nb + j) * epi.ldct + m, v[j], epi.out_bf16);
         }
     }
+}
+
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Full 16-column chunk, mode and output type fixed at compile time: bias read
+// with four 16-byte broadcast loads when aligned, hardware tanh when the output
+// is bf16 (tanh.approx's 2^-10.7 relative error is below bf16's half ulp), and
+// C^T written by pointer increment (one coalesced 64-byte warp segment per
+// column). No per-element bounds checks.
+template <int MODE, bool BF>
+__device__ __forceinline__ void epi_chunk_fast(const EpiArgs& epi, uint64_t m, uint64_t nb, const uint32_t (&r)[16],
+                                               bool vec_c, bool vec_act, bool vec_bias, bool have_pre, uint4 pre0,
+                                               uint4 pre1) {
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+    if constexpr (MODE == EPI_BIAS || MODE == EPI_BIAS_TANH) {
+        float b[16];
+        if (vec_bias) {
+            const float4* bp = reinterpret_cast<const float4*>(epi.bias + nb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float4 f = __ldg(bp + j);
+                b[4 * j] = f.x, b[4 * j + 1] = f.y, b[4 * j + 2] = f.z, b[4 * j + 3] = f.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) b[j] = __ldg(epi.bias + nb + j);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            v[j] += b[j];
+            if constexpr (MODE == EPI_BIAS_TANH) v[j] = BF ? tanh_fast(v[j]) : tanhf(v[j]);
+        }
+    } else if constexpr (MODE == EPI_TANH_GRAD) {
+        float a[16];
+        if (vec_act) {
+            if constexpr (BF) {
+                const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact + nb);
+                uint4 u[2];
+                if (have_pre) u[0] = pre0, u[1] = pre1;  // prefetched by the caller
+                else u[0] = src[0], u[1] = src[1];
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(u);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) a[j] = __bfloat162float(h[j]);
+            } else {
+                const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(epi.act) + m * epi.ldact + nb);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 f = src[j];
+                    a[4 * j] = f.x, a[4 * j + 1] = f.y, a[4 * j + 2] = f.z, a[4 * j + 3] = f.w;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = load_act(epi, m, nb + j);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = v[j] * (1.0f - a[j] * a[j]);
+    }
+    if constexpr (BF) {
+        uint32_t p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            p[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        if (epi.c) {
+            __nv_bfloat16* row = static_cast<__nv_bfloat16*>(epi.c) + m * epi.ldc + nb;
+            if (vec_c) {
+                uint4* dst = reinterpret_cast<uint4*>(row);
+                dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+                dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+            } else {
+                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(p);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) row[j] = h[j];
+            }
+        }
+        if (epi.ct) {
+            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(p);
+            __nv_bfloat16* col = static_cast<__nv_bfloat16*>(epi.ct) + nb * epi.ldct + m;
+#pragma unroll
+            for (int j = 0; j < 16; ++j, col += epi.ldct) *col = h[j];
+        }
+    } else {
+        if (epi.c) {
+            float* row = static_cast<float*>(epi.c) + m * epi.ldc + nb;
+            if (vec_c) {
+                float4* dst = reinterpret_cast<float4*>(row);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) row[j] = v[j];
+            }
+        }
+        if (epi.ct) {
+            float* col = static_cast<float*>(epi.ct) + nb * epi.ldct + m;
+#pragma unroll
+            for (int j = 0; j < 16; ++j, col += epi.ldct) *col = v[j];
+        }
+    }
+}
+
+__device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64_t nb, uint64_t N,
+                                          const uint32_t (&r)[16], bool vec_c, bool vec_act, bool have_pre, uint4 pre0,
+                                          uint4 pre1) {
+    if (nb + 16 > N) {
+        epi_chunk_generic(epi, m, nb, N, r, vec_c, vec_act);
+        return;
+    }
+    const bool vec_bias = epi.bias && ((reinterpret_cast<uintptr_t>(epi.bias + nb) & 15) == 0);
+#define SYNK_EPI_CASE(MODE)                                                       \
+    case MODE:                                                                    \
+        if (epi.out_bf16) epi_chunk_fast<MODE, true>(epi, m, nb, r, vec_c, vec_act, vec_bias, have_pre, pre0, pre1); \
+        else epi_chunk_fast<MODE, false>(epi, m, nb, r, vec_c, vec_act, vec_bias, have_pre, pre0, pre1); \
+        return;
+    switch (epi.mode) {
+        SYNK_EPI_CASE(EPI_STORE)
+        SYNK_EPI_CASE(EPI_BIAS)
+        SYNK_EPI_CASE(EPI_BIAS_TANH)
+        SYNK_EPI_CASE(EPI_TANH_GRAD)
+    }
+#undef SYNK_EPI_CASE
+    epi_chunk_generic(epi, m, nb, N, r, vec_c, vec_act);
 }
 
 // ---- persistent bf16 kernel: 128 x 256 tiles, double-buffered TMEM accumulators -------
@@ -446,11 +601,18 @@ __global__ void __launch_bounds__(PThreads, 1)
             tc_fence_after();
             const uint64_t m = m0 + quad * 32 + lane;
             const uint32_t base = tmem + acc * PBN + ((uint32_t)(quad * 32) << 16);
+            const int cbeg = half * (PBN / 2), cend = cbeg + PBN / 2;
+            ActPrefetch pf{epi.mode == EPI_TANH_GRAD && epi.out_bf16 && vec_act && m < M,
+                           static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact, {}};
+            if (pf.on && n0 + cbeg + 16 <= N) pf.load(n0 + cbeg);
 #pragma unroll 1
-            for (int c0 = half * (PBN / 2); c0 < (half + 1) * (PBN / 2); c0 += 16) {
+            for (int c0 = cbeg; c0 < cend; c0 += 16) {
+                const uint4 cur0 = pf.buf[0], cur1 = pf.buf[1];
+                const bool have = pf.on && n0 + c0 + 16 <= N;
+                if (pf.on && c0 + 16 < cend && n0 + c0 + 32 <= N) pf.load(n0 + c0 + 16);
                 uint32_t r[16];
                 tmem_ld16(base + c0, r);
-                if (m < M && n0 + c0 < N) epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act);
+                if (m < M && n0 + c0 < N) epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act, have, cur0, cur1);
             }
             tc_fence_before();
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
@@ -505,7 +667,8 @@ constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*
 
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-           const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e) {
+           const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
+           uint32_t kb_per = 0x7fffffffu) {
     static bool attr_set[2][2] = {{false, false}, {false, false}};
     // Epilogue-heavy launches (short K, or the tanh-derivative reading the
     // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
@@ -515,21 +678,21 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
         return e ? atoi(e) : 0;
     }();
     const bool wide = forced ? forced == 8 : (K <= 512 || e.mode == EPI_TANH_GRAD);
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), splits);
     if (wide) {
         if (!attr_set[KIND][1]) {
             SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
             attr_set[KIND][1] = true;
         }
         gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e);
+                                                                       (uint32_t)K, e, kb_per);
     } else {
         if (!attr_set[KIND][0]) {
             SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
             attr_set[KIND][0] = true;
         }
         gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e);
+                                                                       (uint32_t)K, e, kb_per);
     }
     SYNK_LAUNCHED("gemm_tc_kernel");
     return SYNK_OK;
@@ -581,9 +744,100 @@ __global__ void __launch_bounds__(256) prep_kernel(const In* __restrict__ in, ui
     }
 }
 
+// Split-K fold: C[m, n] = sum_z P[z][m, n] (fixed z order, f64 accumulation)
+// + bias[n] for EPI_BIAS; fp32 output.
+__global__ void __launch_bounds__(256) splitk_fold_kernel(uint32_t S, uint64_t M, uint64_t N, const float* __restrict__ P,
+                                                          float* __restrict__ C, uint64_t ldc, const float* __restrict__ bias) {
+    const uint64_t total = M * N;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
+        double acc = 0.0;
+        for (uint32_t z = 0; z < S; ++z) acc += (double)P[(uint64_t)z * total + i];
+        const uint64_t m = i / N, n = i % N;
+        float v = (float)acc;
+        if (bias) v += bias[n];
+        C[m * ldc + n] = v;
+    }
+}
+
+// One read, two bf16 writes: out = bf16(in) (rows x cols, ld_out) and
+// out_t = bf16(in)^T (cols x rows, ld_out_t); either may be null. 64 x 64
+// tiles: float4 loads and 8-byte bf16 stores row-major, 32-byte stores for
+// the transposed side out of a shared-memory tile.
+__global__ void __launch_bounds__(256) prep2_bf16_kernel(const float* __restrict__ in, uint64_t rows, uint64_t cols,
+                                                         uint64_t ld_in, __nv_bfloat16* __restrict__ out,
+                                                         uint64_t ld_out, __nv_bfloat16* __restrict__ out_t,
+                                                         uint64_t ld_out_t, int vec_in) {
+    __shared__ float tile[64][65];
+    const uint64_t r0 = (uint64_t)blockIdx.y * 64, c0 = (uint64_t)blockIdx.x * 64;
+    const int t = threadIdx.x;
+    const int lc = (t % 16) * 4;  // 4 consecutive columns
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+        const int lr = t / 16 + 16 * pass;
+        const uint64_t r = r0 + lr, c = c0 + lc;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (r < rows) {
+            if (vec_in && c + 4 <= cols) {
+                const float4 f = __ldcs(reinterpret_cast<const float4*>(in + r * ld_in + c));
+                v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c + j < cols) v[j] = in[r * ld_in + c + j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tile[lr][lc + j] = v[j];
+        if (out && r < rows) {
+            __nv_bfloat16 h[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) h[j] = __float2bfloat16_rn(v[j]);
+            __nv_bfloat16* dst = out + r * ld_out + c;
+            if (c + 4 <= cols && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+                *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c + j < cols) dst[j] = h[j];
+            }
+        }
+    }
+    if (!out_t) return;
+    __syncthreads();
+    // transposed: thread -> output row c0 + t/4, 16 consecutive input rows
+    const int oc = t / 4, seg = (t % 4) * 16;
+    const uint64_t orow = c0 + oc;
+    if (orow >= cols) return;
+    __align__(16) __nv_bfloat16 h[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) h[j] = __float2bfloat16_rn(tile[seg + j][oc]);
+    const uint64_t ocol = r0 + seg;
+    __nv_bfloat16* dst = out_t + orow * ld_out_t + ocol;
+    if (ocol + 16 <= rows && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(h)[0];
+        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(h)[1];
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (ocol + j < rows) dst[j] = h[j];
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+int synk_gemm_prep2_bf16(synk_dev* d, const float* in, uint64_t rows, uint64_t cols, uint64_t ld_in, void* out,
+                         uint64_t ld_out, void* out_t, uint64_t ld_out_t) {
+    if (rows == 0 || cols == 0 || (!out && !out_t)) return SYNK_OK;
+    synk::DeviceGuard g(d->device);
+    dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
+    const int vec_in = (ld_in % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
+    prep2_bf16_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out), ld_out,
+                                                   static_cast<__nv_bfloat16*>(out_t), ld_out_t, vec_in);
+    SYNK_LAUNCHED("prep2_bf16_kernel");
+    return SYNK_OK;
+}
 
 int synk_gemm_prep(synk_dev* d, int in_dtype, const void* in, uint64_t rows, uint64_t cols, uint64_t ld_in,
                    int transpose, int mode, void* out_hi, float* out_lo, uint64_t out_rows, uint64_t out_cols,
@@ -624,11 +878,14 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
     EpiArgs e{epilogue, out_dtype == 3, c, ldc, ct, ldct, bias, act, ldact};
     if (K == 0) return synk::fail(SYNK_EARG, "gemm_tc: K must be > 0");
     // Wide bf16 problems: persistent 128x256 tiles (SYNK_GEMM_PERSISTENT=0 disables).
-    static const bool persistent_ok = [] {
+    // Every bf16 product with N > 128 (short-K, epilogue-bound ones included:
+    // the persistent kernel overlaps tile i's epilogue with tile i+1's loads).
+    // SYNK_GEMM_PERSISTENT=0 disables it (A/B diagnostics).
+    static const int persistent_mode = [] {
         const char* v = getenv("SYNK_GEMM_PERSISTENT");
-        return !(v && v[0] == '0');
+        return v ? atoi(v) : 1;
     }();
-    if (bf16 && persistent_ok && N > 128 && K > 256) {
+    if (bf16 && persistent_mode && N > 128) {
         CUtensorMap bw;
         if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
         constexpr size_t smem = (size_t)PStages * (PA + PB) + 1024 + 256;
@@ -641,6 +898,35 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
         gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e);
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
+        return SYNK_OK;
+    }
+    // Too few output tiles to fill the GPU and a long K: split K over grid.z
+    // (fixed split for a given shape, so results do not depend on the device),
+    // fp32 partial planes in a stream-ordered scratch, one fold kernel.
+    const uint64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const uint32_t kBKe = bf16 ? 64 : 32;
+    const uint64_t num_kb = (K + kBKe - 1) / kBKe;
+    uint32_t splits = 1;
+    if (tiles < 148 && num_kb >= 16 && (epilogue == SYNK_EPI_STORE || epilogue == SYNK_EPI_BIAS) &&
+        out_dtype == SYNK_F32 && !ct && c) {
+        uint64_t sp = 296 / tiles;  // one wave of 2 CTAs per SM
+        sp = std::min<uint64_t>(sp, num_kb / 8);
+        splits = (uint32_t)std::max<uint64_t>(sp, 1);
+    }
+    if (splits > 1) {
+        const uint32_t kb_per = (uint32_t)((num_kb + splits - 1) / splits);
+        splits = (uint32_t)((num_kb + kb_per - 1) / kb_per);
+        float* planes = nullptr;
+        SYNK_CU(cudaMallocAsync((void**)&planes, (size_t)splits * M * N * sizeof(float), d->stream));
+        EpiArgs pe{SYNK_EPI_STORE, 0, planes, N, nullptr, 0, nullptr, nullptr, 0};
+        int rc = bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per)
+                      : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per);
+        if (rc) return rc;
+        const unsigned fgrid = (unsigned)std::min<uint64_t>((M * N + 255) / 256, (uint64_t)d->num_sms * 8);
+        splitk_fold_kernel<<<fgrid, 256, 0, d->stream>>>(splits, M, N, planes, static_cast<float*>(c), ldc,
+                                                         epilogue == SYNK_EPI_BIAS ? bias : nullptr);
+        SYNK_LAUNCHED("splitk_fold_kernel");
+        SYNK_CU(cudaFreeAsync(planes, d->stream));
         return SYNK_OK;
     }
     return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e)

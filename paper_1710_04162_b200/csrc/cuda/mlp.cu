@@ -205,13 +205,20 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
-__global__ void loss_final_kernel(const double* __restrict__ partial, int count, double scale,
-                                  double* __restrict__ loss) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < count; ++i) s += partial[i];
-        *loss = s * scale;  // mlp.cpp:190: loss *= 0.5 * inv_n
+// Fixed-order fold of the per-CTA partials: thread t sums partials t, t+256, ...
+// then a fixed shared-memory tree (deterministic).
+__global__ void __launch_bounds__(256) loss_final_kernel(const double* __restrict__ partial, int count, double scale,
+                                                         double* __restrict__ loss) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += 256) s += partial[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + w];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *loss = red[0] * scale;  // mlp.cpp:190: loss *= 0.5 * inv_n
 }
 
 // gb[j] = sum_i delta[i, j]  (f64 accumulation, deterministic row order per column block)
@@ -259,7 +266,7 @@ int make_plan(const uint64_t* dims, uint32_t layers, uint64_t n, Plan* p) {
     return SYNK_OK;
 }
 
-constexpr int kLossBlocks = 128;
+constexpr int kLossBlocks = 592;  // 4 CTAs per SM of a B200
 
 // workspace: acts[1..L] | delta ping | delta pong | loss partials | split-K partials
 uint64_t ws_bytes(int dtype, const Plan& p, uint64_t n) {
@@ -304,7 +311,7 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     double inv_n = 1.0 / (double)n;
     loss_delta_kernel<T><<<blocks, kThreads, 0, d->stream>>>(acts[layers], y, n_el, inv_n, dA, partial);
     SYNK_LAUNCHED("loss_delta_kernel");
-    loss_final_kernel<<<1, 32, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
+    loss_final_kernel<<<1, 256, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
     SYNK_LAUNCHED("loss_final_kernel");
 
     T* delta = dA;
@@ -401,24 +408,17 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
     const int F32 = SYNK_F32, BF = SYNK_BF16;
 
-    // weights: W_l (K-major for dX) and W_l^T (K-major for the forward)
+    // weights: W_l (K-major for dX) and W_l^T (K-major for the forward), one read each
     for (uint32_t l = 0; l < L; ++l) {
         const float* W = theta + P.woff[l];
-        if (int rc = synk_gemm_prep(d, F32, W, dims[l], dims[l + 1], dims[l + 1], 0, 1, bf(B.off_w[l]), nullptr,
-                                    dims[l], dims[l + 1], pad8(dims[l + 1]));
-            rc)
-            return rc;
-        if (int rc = synk_gemm_prep(d, F32, W, dims[l], dims[l + 1], dims[l + 1], 1, 1, bf(B.off_wt[l]), nullptr,
-                                    dims[l + 1], dims[l], pad8(dims[l]));
+        if (int rc = synk_gemm_prep2_bf16(d, W, dims[l], dims[l + 1], dims[l + 1], bf(B.off_w[l]), pad8(dims[l + 1]),
+                                          bf(B.off_wt[l]), pad8(dims[l]));
             rc)
             return rc;
     }
     // input batch: x and x^T in bf16
-    if (int rc = synk_gemm_prep(d, F32, x, n, dims[0], dims[0], 0, 1, bf(B.off_act[0]), nullptr, n, dims[0],
-                                pad8(dims[0]));
-        rc)
-        return rc;
-    if (int rc = synk_gemm_prep(d, F32, x, n, dims[0], dims[0], 1, 1, bf(B.off_actT[0]), nullptr, dims[0], n, pad8(n));
+    if (int rc = synk_gemm_prep2_bf16(d, x, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]), bf(B.off_actT[0]),
+                                      pad8(n));
         rc)
         return rc;
 
@@ -442,12 +442,11 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     const double inv_n = 1.0 / (double)n;
     loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial);
     SYNK_LAUNCHED("loss_delta_kernel");
-    loss_final_kernel<<<1, 32, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
+    loss_final_kernel<<<1, 256, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
     SYNK_LAUNCHED("loss_final_kernel");
     int cur = 0;
-    if (int rc = synk_gemm_prep(d, F32, delta_f, n, dl, dl, 0, 1, bf(B.off_d[cur]), nullptr, n, dl, pad8(P.maxd)); rc)
-        return rc;
-    if (int rc = synk_gemm_prep(d, F32, delta_f, n, dl, dl, 1, 1, bf(B.off_dT[cur]), nullptr, dl, n, pad8(n)); rc)
+    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd), bf(B.off_dT[cur]), pad8(n));
+        rc)
         return rc;
     // output-layer bias grad: row-chunked column sums (f64 accumulation), enough CTAs for large n
     if (int rc = synk_column_stats(d, F32, delta_f, n, dl, grad + P.boff[L - 1], nullptr, nullptr); rc) return rc;

@@ -43,6 +43,20 @@ with sk.Pool(workers=1) as pool:
         gaps.append((b.time_range.start - a.time_range.end, a.name[:50], b.name[:50]))
     for gp in sorted(gaps, reverse=True)[:8]:
         print("gap %10.1f us  after %s  before %s" % gp)
+    t_end = max(e.time_range.end for e in evs)
+    last = [e for e in sorted(evs, key=lambda e: e.time_range.start) if e.time_range.start >= t_end - 1500]
+    print("---- launches of the last ~1.5 ms ----")
+    for e in last:
+        print("%8.1f %8.1f  %s" % (e.time_range.start - last[0].time_range.start, e.time_range.end - e.time_range.start,
+                                    e.name[:70]))
+    agg_k = {}
+    for e in evs:
+        a = agg_k.setdefault(e.name[:70], [0, 0.0])
+        a[0] += 1
+        a[1] += e.time_range.end - e.time_range.start
+    print("---- device time per step by kernel ----")
+    for k, (c, t) in sorted(agg_k.items(), key=lambda kv: -kv[1][1])[:25]:
+        print("%9.1f us/step  n/step=%5.1f  %s" % (t / 12, c / 12, k))
     cpu = [e for e in prof.events() if e.device_type.name == "CPU"]
     agg = {}
     for e in cpu:

@@ -48,8 +48,20 @@ def run(R, name, M, N, K, epi, out_bf16, with_ct, with_act, reps=10):
                                                                               2.0 * M * N * K / t / 1e12))
 
 
+only = sys.argv[1] if len(sys.argv) > 1 else None
+_run = run
+
+
+def run(R, name, *a, **k):  # noqa: F811
+    if only is None or name.startswith(only):
+        _run(R, name, *a, **k)
+
+
 with Ranks(1) as R:
     n = 8192
+    run(R, "fwd1 store bf16", n, 4096, 4096, 0, True, False, False)
+    run(R, "fwd1 bias_tanh", n, 4096, 4096, 2, True, False, False)
+    run(R, "fwd1 store bf16+ct", n, 4096, 4096, 0, True, True, False)
     run(R, "fwd0 bias_tanh+ct", n, 4096, 2048, 2, True, True, False)
     run(R, "fwd1 bias_tanh+ct", n, 4096, 4096, 2, True, True, False)
     run(R, "fwd2 bias f32", n, 100, 4096, 1, False, False, False)

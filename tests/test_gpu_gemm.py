@@ -153,3 +153,40 @@ def test_bf16_tensor_core_mlp_vs_oracle(sk, oracle, world):
         # parallel call: shard-mean gradients, row-weighted loss (same bar)
         (ploss,) = f.call([x, y])
         assert abs(ploss - ref_loss) / ref_loss <= 1e-2
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(8192, 100, 4096, "bias"), (4096, 100, 8192, "store"), (300, 64, 2000, "bias")])
+def test_bf16_split_k_small_n(M, N, K, epi):
+    """Few output tiles + long K take the split-K path (fp32 partial planes,
+    fixed-order fold with the bias): same accuracy bar as the unsplit kernel,
+    and run-to-run bitwise deterministic."""
+    rng = np.random.default_rng(M + N + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)))
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    if epi == "bias":
+        want = want + bias
+    with Ranks(1) as R:
+        got, _ = gemm(R, "bf16", a, b, epi, bias if epi == "bias" else None)
+        again, _ = gemm(R, "bf16", a, b, epi, bias if epi == "bias" else None)
+    assert rel_err(got, want) <= 1e-6 + 5e-8 * K
+    assert got.tobytes() == again.tobytes()
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 64), (1000, 100), (37, 5), (130, 2048)])
+def test_prep2_bf16_cast_and_transpose(rows, cols):
+    rng = np.random.default_rng(rows * cols)
+    x = rng.uniform(-3, 3, (rows, cols)).astype(np.float32)
+    ld, ldt = pad(cols, 8), pad(rows, 8)
+    want = bf16_round(x).view(np.uint32) >> 16
+    with Ranks(1) as R:
+        dx = R.upload(x)
+        o, ot = R.alloc(rows * ld * 2), R.alloc(cols * ldt * 2)
+        check(lib().synk_gemm_prep2_bf16(R[0], _vp(dx), _u64(rows), _u64(cols), _u64(cols), _vp(o), _u64(ld), _vp(ot),
+                                         _u64(ldt)), "prep2")
+        check(R.sync(), "sync")
+        got = R.download(o, (rows, ld), np.uint16)[:, :cols]
+        got_t = R.download(ot, (cols, ldt), np.uint16)[:, :rows]
+    np.testing.assert_array_equal(got, want.astype(np.uint16))
+    np.testing.assert_array_equal(got_t, want.T.astype(np.uint16))
