@@ -18,6 +18,10 @@ shuffled 4096-row batches from a 10M x 256 fp32 shared dataset.
            on this box's cores, bounded sample of the same workload.
   sync_sgd C1 (784-512-10 fp32 MLP, batch 256/GPU indexed, grad all-reduce
            mean fused with the SGD update), samples/s through Trainer.
+  sync_sgd_wide_bf16  C5 (2048-4096-4096-100, bf16 tcgen05 GEMMs, 8192/GPU).
+  slicing_c3  C3: column sums + maxima (+ Gather) over an 8M x 1024 fp32
+           HBM-resident input, num_slices=4, vs the HBM roofline.
+  collectives_c4  C4: all-reduce mean + broadcast sweep 1 KiB - 1 GiB.
 
 `--impl reference` times only the reference CPU implementation on the same
 config and prints its line. Under torchrun (N>1) the synkpar executor is one
@@ -195,6 +199,13 @@ def workload_config(args, n_gpus):
         "rows_per_step": args.batch * args.batches * n_gpus, "row_bytes": args.cols * 4,
         "parallelism": "dp%d (one rank per GPU, single-process executor)" % n_gpus,
         "l2": "inputs larger than L2 (10.24 GB dataset, 2 rotating 256 MiB outputs per GPU)"}
+
+
+def pinned_indexes(sk, rng, rows, n):
+    """A step's index list in pinned host memory (what a data loader hands over)."""
+    buf = sk.pinned_array(n, "int64")
+    buf[:] = rng.integers(0, rows, n)
+    return buf
 
 
 def fill_dataset(sk, rows, cols):
@@ -443,7 +454,7 @@ def ours(args, n_gpus):
         g = sk.mlp_grad_function(pool, block)
         sk.distribute(pool)
         tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
-        sel = [rng.integers(0, 65536, 256 * n_gpus) for _ in range(total_steps)]
+        sel = [pinned_indexes(sk, rng, 65536, 256 * n_gpus) for _ in range(total_steps)]
         for s in range(args.warmup):
             tr.train_step(g, [sx, sy], indexes=sel[s])
         t0 = time.perf_counter()
@@ -470,7 +481,7 @@ def ours(args, n_gpus):
         sk.distribute(pool)
         tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
         per_gpu = 8192
-        sel = [rng.integers(0, 16384, per_gpu * n_gpus) for _ in range(total_steps)]
+        sel = [pinned_indexes(sk, rng, 16384, per_gpu * n_gpus) for _ in range(total_steps)]
         for s in range(args.warmup):
             tr.train_step(g, [sx, sy], indexes=sel[s])
         t0 = time.perf_counter()

@@ -349,20 +349,18 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
 
 inline uint64_t pad8(uint64_t v) { return (v + 7) / 8 * 8; }
 
-// out[r] = sum_j in[r * ld + j], j < n (bf16 in, f32 out, f64 accumulation).
-__global__ void __launch_bounds__(256) rowsum_bf16_kernel(const __nv_bfloat16* __restrict__ in, uint64_t ld, uint64_t n,
-                                                           float* __restrict__ out) {
-    __shared__ double red[256];
-    const __nv_bfloat16* row = in + (uint64_t)blockIdx.x * ld;
-    double s = 0.0;
-    for (uint64_t j = threadIdx.x; j < n; j += 256) s += (double)__bfloat162float(row[j]);
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) out[blockIdx.x] = (float)red[0];
+// Row `row` of each a_l^T buffer = 1.0 (bf16), so the weight-gradient GEMM
+// over M = d_l + 1 rows also yields sum_i delta[i, :] = the bias gradient,
+// landing on b_l right after W_l in the flat parameter layout.
+struct OnesRows {
+    __nv_bfloat16* p[64];
+    uint32_t count;
+};
+__global__ void __launch_bounds__(256) ones_rows_kernel(OnesRows rows, uint64_t n) {
+    const __nv_bfloat16 one = __float2bfloat16_rn(1.0f);
+    for (uint32_t l = blockIdx.y; l < rows.count; l += gridDim.y)
+        for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256)
+            rows.p[l][i] = one;
 }
 
 struct Bf16Plan {
@@ -388,7 +386,7 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
     }
     for (uint32_t l = 0; l < L; ++l) {  // act[0] = x, act[l] hidden
         p.off_act[l] = take(n * pad8(dims[l]) * 2);
-        p.off_actT[l] = take(dims[l] * pad8(n) * 2);
+        p.off_actT[l] = take((dims[l] + 1) * pad8(n) * 2);  // + a row of ones (bias gradient)
     }
     p.off_pred = take(n * dims[L] * 4);
     p.off_delta_f = take(n * dims[L] * 4);
@@ -422,6 +420,14 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         rc)
         return rc;
 
+    {
+        OnesRows o{};
+        o.count = L;
+        for (uint32_t l = 0; l < L; ++l) o.p[l] = bf(B.off_actT[l]) + dims[l] * pad8(n);
+        ones_rows_kernel<<<dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 64), L), 256, 0, d->stream>>>(o, n);
+        SYNK_LAUNCHED("ones_rows_kernel");
+    }
+
     // forward
     float* pred = reinterpret_cast<float*>(base + B.off_pred);
     for (uint32_t l = 0; l < L; ++l) {
@@ -448,22 +454,16 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd), bf(B.off_dT[cur]), pad8(n));
         rc)
         return rc;
-    // output-layer bias grad: row-chunked column sums (f64 accumulation), enough CTAs for large n
-    if (int rc = synk_column_stats(d, F32, delta_f, n, dl, grad + P.boff[L - 1], nullptr, nullptr); rc) return rc;
 
     // backward
     for (uint32_t l = L; l-- > 0;) {
         const uint64_t din = dims[l], dout = dims[l + 1];
-        // gW_l = a_l^T . delta  (M = din, N = dout, K = n)
-        if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, din, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), bf(B.off_dT[cur]),
+        // [gW_l; gb_l] = [a_l^T; 1] . delta  (M = din + 1: the last row is the bias gradient)
+        if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, din + 1, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), bf(B.off_dT[cur]),
                                   nullptr, pad8(n), SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr,
                                   nullptr, 0);
             rc)
             return rc;
-        if (l + 1 < L) {  // hidden-layer bias grads from delta^T rows
-            rowsum_bf16_kernel<<<(unsigned)dout, 256, 0, d->stream>>>(bf(B.off_dT[cur]), pad8(n), n, grad + P.boff[l]);
-            SYNK_LAUNCHED("rowsum_bf16_kernel");
-        }
         if (l > 0) {
             // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
             const int nxt = cur ^ 1;
