@@ -109,6 +109,13 @@ int synk_copy2d(synk_dev* dev, void* dst, uint64_t dpitch, const void* src, uint
 int synk_memset(synk_dev* dev, void* dst, int value, uint64_t bytes);
 /* Fill n elements with a value (NdBuffer::fill, tensor.cpp:141-151). */
 int synk_fill(synk_dev* dev, int dtype, void* dst, double value, uint64_t n);
+
+/* dst[0:bytes] = src[0:bytes] by one CTA of the rank's SMs (bytes <= 1 MiB),
+ * async on the rank stream. For small results headed to mapped pinned host
+ * memory: the phase's last kernel writes them over PCIe instead of a separate
+ * copy-engine D2H after the phase (replaces the NdBuffer copy-out of
+ * function.cpp:515-527 for a single contributor). */
+int synk_copy_small(synk_dev* dev, void* dst, const void* src, uint64_t bytes);
 /* Synthetic data generated in place (no reference counterpart: replaces the
  * host-side dataset generation + H2D of bench.cpp:41-58 / acceptance C3 for
  * HBM-resident inputs). Element i of dst = U[-1,1) value number first+i of

@@ -116,6 +116,10 @@ struct CallOptions {
     // stay valid and unmodified for the duration of the call.
     const std::uint64_t* index_view = nullptr;
     std::size_t index_view_count = 0;
+    // Fill CallReport::scatter_s / rank_compute_s from device events. A caller
+    // that discards the report (Python Function.call) sets false and saves the
+    // event records and elapsed-time queries of every call.
+    bool device_timing = true;
 };
 
 struct CallReport {

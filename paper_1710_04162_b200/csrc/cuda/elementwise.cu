@@ -447,6 +447,33 @@ int synk_scale(synk_dev* d, int dtype, void* buf, double factor, uint64_t n) {
     return SYNK_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Small copies by the SMs (one CTA): into mapped pinned host memory the
+// stores are posted PCIe writes, cheaper than a copy-engine round trip.
+__global__ void copy_small_kernel(char* __restrict__ dst, const char* __restrict__ src, uint64_t bytes) {
+    const bool v16 = ((uintptr_t)dst | (uintptr_t)src | bytes) % 16 == 0;
+    if (v16) {
+        for (uint64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+            reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+        for (uint64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int synk_copy_small(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
+    if (bytes == 0) return SYNK_OK;
+    SYNK_REQUIRE(bytes <= (1u << 20), SYNK_EARG, "synk_copy_small: at most 1 MiB");
+    synk::DeviceGuard g(d->device);
+    copy_small_kernel<<<1, 256, 0, d->stream>>>((char*)dst, (const char*)src, bytes);
+    SYNK_LAUNCHED("copy_small_kernel");
+    return SYNK_OK;
+}
+
 int synk_fill(synk_dev* d, int dtype, void* dst, double value, uint64_t n) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_fill: bad dtype");
     if (n == 0) return SYNK_OK;

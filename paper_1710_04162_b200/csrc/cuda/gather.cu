@@ -1,7 +1,8 @@
 // Input indexing: dst[j,:] = src[idx[j],:]   (gather_rows, tensor.cpp:200-217)
 //
-// HBM-bound row gather. One warp owns ROWS destination rows at a time: lanes
-// < ROWS fetch the indices, shuffle them to the warp, then every lane streams
+// HBM-bound row gather. One warp owns a contiguous block of destination rows
+// and works on ROWS of them at a time: the indices are shuffled to the warp,
+// then every lane streams
 // 16-byte vectors of all ROWS rows (ROWS x UNROLL independent 128-bit loads in
 // flight per lane before the first store), so a 1 KiB row is two fully
 // coalesced 512-byte warp transactions per row and no shared memory is
@@ -9,6 +10,8 @@
 // touched once); the source may be an HBM mirror or pinned, mapped host memory
 // (then the same loads travel over PCIe). Out-of-range indices set the rank's
 // device error flag, reported as BoundsError at the phase-exit synk_sync().
+
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -53,47 +56,64 @@ constexpr int kRows = 4;    // rows in flight per warp
 constexpr int kUnroll = 2;  // vectors per row in flight per lane
 constexpr int kBlock = 256;
 
+// Chunked grid-stride: warp w takes chunks w, w + nwarps, ... of `chunk`
+// consecutive destination rows (chunk <= 32, a multiple of kRows), so warps
+// running at the same time write neighbouring rows of dst. Lane i < chunk
+// holds index i of the chunk (one coalesced read, which matters when the list
+// sits in pinned host memory and travels over PCIe), and the NEXT chunk's
+// indices are requested before the current chunk's rows are streamed, so the
+// index fetch overlaps a chunk of row traffic.
 template <int BYTES>
 __global__ void __launch_bounds__(kBlock) gather_rows_kernel(
     const typename Vec<BYTES>::T* __restrict__ src, uint64_t src_rows, uint64_t row_vecs,
-    const uint64_t* __restrict__ idx, uint64_t n_idx, typename Vec<BYTES>::T* __restrict__ dst,
+    const uint64_t* __restrict__ idx, uint64_t n_idx, uint32_t chunk, typename Vec<BYTES>::T* __restrict__ dst,
     int* __restrict__ err) {
     using V = typename Vec<BYTES>::T;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+    const uint64_t stride = (((uint64_t)gridDim.x * kBlock) >> 5) * chunk;
+    if (src_rows == 0) {  // every index is out of range
+        if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)err = 1;
+        return;
+    }
 
-    for (uint64_t r0 = warp * kRows; r0 < n_idx; r0 += nwarps * kRows) {
-        uint64_t mine = 0;
-        int ok = 0;
-        if (lane < kRows && r0 + lane < n_idx) {
-            mine = idx[r0 + lane];
-            ok = mine < src_rows;
-            if (!ok) *(volatile int*)err = 1;  // mapped host flag: plain store, every writer stores 1
-        }
-        uint64_t row[kRows];
-        int valid[kRows];
+    uint64_t c0 = warp * chunk;
+    uint64_t next = c0 + lane < n_idx && lane < (int)chunk ? idx[c0 + lane] : 0;
+    for (; c0 < n_idx; c0 += stride) {
+        const uint64_t mine = next;
+        const int in_chunk = (int)(n_idx - c0 < chunk ? n_idx - c0 : chunk);
+        const uint64_t cn = c0 + stride;
+        if (lane < (int)chunk && cn + lane < n_idx) next = idx[cn + lane];  // prefetch the next chunk
+        const int ok = lane < in_chunk && mine < src_rows;
+        if (lane < in_chunk && !ok) *(volatile int*)err = 1;  // mapped host flag: every writer stores 1
+        for (int g = 0; g < in_chunk; g += kRows) {
+            // A bad index reads row 0 instead (defined data; the call fails).
+            const uint64_t safe = ok ? mine : 0;
+            uint64_t row[kRows];
+            int exists[kRows];
 #pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-            row[k] = __shfl_sync(0xffffffffu, mine, k);
-            valid[k] = __shfl_sync(0xffffffffu, ok, k);
-        }
-        for (uint64_t v0 = lane; v0 < row_vecs; v0 += 32 * kUnroll) {
-            V buf[kRows][kUnroll];
+            for (int k = 0; k < kRows; ++k) {
+                row[k] = __shfl_sync(0xffffffffu, safe, (g + k) & 31);
+                exists[k] = g + k < in_chunk;
+            }
+            const uint64_t r0 = c0 + g;
+            for (uint64_t v0 = lane; v0 < row_vecs; v0 += 32 * kUnroll) {
+                V buf[kRows][kUnroll];
 #pragma unroll
-            for (int k = 0; k < kRows; ++k)
+                for (int k = 0; k < kRows; ++k)
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    uint64_t v = v0 + (uint64_t)u * 32;
-                    if (valid[k] && v < row_vecs) buf[k][u] = Vec<BYTES>::load(src + row[k] * row_vecs + v);
-                }
+                    for (int u = 0; u < kUnroll; ++u) {
+                        uint64_t v = v0 + (uint64_t)u * 32;
+                        if (exists[k] && v < row_vecs) buf[k][u] = Vec<BYTES>::load(src + row[k] * row_vecs + v);
+                    }
 #pragma unroll
-            for (int k = 0; k < kRows; ++k)
+                for (int k = 0; k < kRows; ++k)
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    uint64_t v = v0 + (uint64_t)u * 32;
-                    if (valid[k] && v < row_vecs) dst[(r0 + k) * row_vecs + v] = buf[k][u];
-                }
+                    for (int u = 0; u < kUnroll; ++u) {
+                        uint64_t v = v0 + (uint64_t)u * 32;
+                        if (exists[k] && v < row_vecs) dst[(r0 + k) * row_vecs + v] = buf[k][u];
+                    }
+            }
         }
     }
 }
@@ -102,14 +122,163 @@ template <int BYTES>
 int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
            const uint64_t* idx, uint64_t n_idx, void* dst) {
     using V = typename Vec<BYTES>::T;
-    uint64_t warps = (n_idx + kRows - 1) / kRows;
-    uint64_t blocks = (warps * 32 + kBlock - 1) / kBlock;
-    uint64_t cap = (uint64_t)d->num_sms * 8;
+    static const uint32_t chunk = getenv("SYNK_GATHER_ROWS") ? atoi(getenv("SYNK_GATHER_ROWS")) : 4;
+    // At most 8 CTAs of 8 warps per SM (about 2.7 waves at 3 resident
+    // CTAs/SM: the oversubscription balances the random-row latency).
+    const uint64_t chunks = (n_idx + chunk - 1) / chunk;
+    uint64_t blocks = (chunks * 32 + kBlock - 1) / kBlock;
+    const uint64_t cap = (uint64_t)d->num_sms * 8;
     if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
     gather_rows_kernel<BYTES><<<(unsigned)blocks, kBlock, 0, d->stream>>>(
-        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, (V*)dst, d->err_dev);
+        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, chunk, (V*)dst, d->err_dev);
     SYNK_LAUNCHED("gather_rows_kernel");
+    return SYNK_OK;
+}
+
+// ---- bulk-copy (TMA engine) gather ---------------------------------------------------
+//
+// For 16-byte-aligned rows up to 8 KiB: one warp per CTA, two CTAs per SM. The
+// warp walks chunks of up to 32 rows (chunk c = blockIdx.x + j*gridDim.x);
+// lane i reads index i of the chunk and issues ONE cp.async.bulk global->shared
+// copy of that whole row into stage j % S of a shared-memory ring, all
+// completing on the stage's mbarrier (expect_tx = the chunk's valid bytes).
+// When a stage lands, lane 0 writes the chunk's rows -- contiguous in dst -- with
+// a single cp.async.bulk shared->global store. S-2 chunks of loads stay in
+// flight per CTA (no registers hold row data, so the in-flight depth is set
+// by shared memory, not by the register file), and each chunk's indices are
+// fetched two chunks ahead so a PCIe-resident index list does not stall the
+// issue loop.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+constexpr int kMaxStages = 16;
+
+__global__ void __launch_bounds__(32) gather_rows_bulk_kernel(
+    const char* __restrict__ src, uint64_t src_rows, uint32_t row_bytes, const uint64_t* __restrict__ idx,
+    uint64_t n_idx, uint32_t chunk_rows, uint32_t stages, char* __restrict__ dst, int* __restrict__ err) {
+    extern __shared__ __align__(128) char ring[];
+    __shared__ __align__(8) uint64_t full[kMaxStages];
+    __shared__ int bad[kMaxStages];
+    const int lane = threadIdx.x;
+    const uint64_t n_chunks = (n_idx + chunk_rows - 1) / chunk_rows;
+    if (blockIdx.x >= n_chunks) return;
+    const uint64_t mine = (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x;  // chunks of this CTA
+    const uint32_t stage_bytes = chunk_rows * row_bytes;
+    if (lane == 0) {
+        for (uint32_t s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    auto chunk_start = [&](uint64_t j) { return (blockIdx.x + j * gridDim.x) * (uint64_t)chunk_rows; };
+    auto load_index = [&](uint64_t j) -> uint64_t {
+        if (j >= mine) return 0;
+        const uint64_t r = chunk_start(j) + lane;
+        return lane < (int)chunk_rows && r < n_idx ? idx[r] : 0;
+    };
+    // Indices two chunks ahead of the issue point.
+    uint64_t q0 = load_index(0), q1 = load_index(1);
+
+    auto issue = [&](uint64_t j, uint64_t my) {
+        const uint32_t s = (uint32_t)(j % stages);
+        const uint64_t r0 = chunk_start(j);
+        const uint32_t cnt = (uint32_t)(n_idx - r0 < chunk_rows ? n_idx - r0 : chunk_rows);
+        const bool live = lane < (int)cnt;
+        const bool ok = live && my < src_rows;
+        const unsigned okm = __ballot_sync(0xffffffffu, ok);
+        const unsigned badm = __ballot_sync(0xffffffffu, live && !ok);
+        char* slot = ring + (size_t)s * stage_bytes + (size_t)lane * row_bytes;
+        if (badm) {  // error path: zero rows for bad indices, flag the rank
+            if (live && !ok) {
+                *(volatile int*)err = 1;
+                for (uint32_t b = 0; b < row_bytes; b += 16) *reinterpret_cast<uint4*>(slot + b) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        if (lane == 0) {
+            bad[s] = badm != 0;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
+                         "r"((uint32_t)__popc(okm) * row_bytes)
+                         : "memory");
+        }
+        __syncwarp();
+        if (ok)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(slot)),
+                "l"(src + my * row_bytes), "r"(row_bytes), "r"(smem_addr(&full[s]))
+                : "memory");
+    };
+
+    const uint64_t ahead = stages - 2 < mine ? stages - 2 : mine;  // chunks in flight before the first store
+    for (uint64_t j = 0; j < ahead; ++j) {
+        issue(j, q0);
+        q0 = q1;
+        q1 = load_index(j + 2);
+    }
+    for (uint64_t j = 0; j < mine; ++j) {
+        const uint32_t s = (uint32_t)(j % stages);
+        bar_wait(smem_addr(&full[s]), (uint32_t)((j / stages) & 1));
+        const uint64_t r0 = chunk_start(j);
+        const uint32_t cnt = (uint32_t)(n_idx - r0 < chunk_rows ? n_idx - r0 : chunk_rows);
+        if (bad[s]) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic zero stores -> async proxy
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + r0 * row_bytes),
+                         "r"(smem_addr(ring + (size_t)s * stage_bytes)), "r"(cnt * row_bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        const uint64_t jn = j + ahead;
+        if (jn < mine) {
+            // Stage jn % S last held chunk jn - S <= j - 2: its store must have
+            // finished reading shared memory (at most the newest group pending).
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            issue(jn, q0);
+            q0 = q1;
+            q1 = load_index(jn + 2);
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int launch_bulk(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes, const uint64_t* idx,
+                uint64_t n_idx, void* dst) {
+    static const uint32_t ctas_per_sm = getenv("SYNK_GATHER_CTAS") ? atoi(getenv("SYNK_GATHER_CTAS")) : 2;
+    static const uint32_t max_chunk = getenv("SYNK_GATHER_CHUNK") ? atoi(getenv("SYNK_GATHER_CHUNK")) : 16;
+    const uint32_t kSmemBudget = (224u * 1024u / ctas_per_sm - 1024u) & ~1023u;  // per CTA
+    uint32_t chunk_rows = max_chunk;
+    while (chunk_rows > 1 && (uint64_t)chunk_rows * row_bytes * 6 > kSmemBudget) chunk_rows /= 2;
+    uint32_t stages = (uint32_t)(kSmemBudget / (chunk_rows * row_bytes));
+    if (stages > kMaxStages) stages = kMaxStages;
+    const uint32_t smem = stages * chunk_rows * (uint32_t)row_bytes;
+    static bool attr_set[64] = {};  // per device (the attribute is per-device state)
+    if (d->device >= 64 || !attr_set[d->device]) {
+        SYNK_CU(cudaFuncSetAttribute(gather_rows_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(224u * 1024u)));
+        if (d->device < 64) attr_set[d->device] = true;
+    }
+    const uint64_t n_chunks = (n_idx + chunk_rows - 1) / chunk_rows;
+    const uint64_t cap = (uint64_t)d->num_sms * ctas_per_sm;
+    const unsigned grid = (unsigned)(n_chunks < cap ? n_chunks : cap);
+    gather_rows_bulk_kernel<<<grid, 32, smem, d->stream>>>((const char*)src, src_rows, (uint32_t)row_bytes, idx,
+                                                           n_idx, chunk_rows, stages, (char*)dst, d->err_dev);
+    SYNK_LAUNCHED("gather_rows_bulk_kernel");
     return SYNK_OK;
 }
 
@@ -121,6 +290,12 @@ extern "C" int synk_gather_rows(synk_dev* d, const void* src, uint64_t src_rows,
     if (n_idx == 0 || row_bytes == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     uint64_t a = row_bytes | (uint64_t)(uintptr_t)src | (uint64_t)(uintptr_t)dst;
+    // Diagnostics: SYNK_GATHER_VEC / SYNK_GATHER_BULK force one kernel (A/B runs).
+    static const bool force_vec = getenv("SYNK_GATHER_VEC") != nullptr;
+    static const bool force_bulk = getenv("SYNK_GATHER_BULK") != nullptr;
+    const bool bulk_ok = (a & 15) == 0 && row_bytes <= 8192;
+    if (bulk_ok && !force_vec && (force_bulk || row_bytes >= 4096))
+        return launch_bulk(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 15) == 0) return launch<16>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 7) == 0) return launch<8>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 3) == 0) return launch<4>(d, src, src_rows, row_bytes, idx, n_idx, dst);

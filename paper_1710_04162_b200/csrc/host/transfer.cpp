@@ -86,12 +86,18 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     if (part.count() == 0 || row_bytes == 0) return out;
     const std::pair<const std::uint64_t*, std::size_t> key{sel.list + part.start, part.count()};
     DevBuffer idx;
-    if (uploads)
-        for (auto& [k, buf] : uploads->done)
-            if (k == key) idx = buf;
-    if (!idx.has_storage()) {
-        idx = upload_indices(rd, key.first, key.second);
-        if (uploads) uploads->done.emplace_back(key, idx);
+    const std::uint64_t* idx_ptr = nullptr;
+    if (is_mapped_host(key.first)) {
+        idx_ptr = key.first;  // pinned list: the gather kernel reads it in place over PCIe
+    } else {
+        if (uploads)
+            for (auto& [k, buf] : uploads->done)
+                if (k == key) idx = buf;
+        if (!idx.has_storage()) {
+            idx = upload_indices(rd, key.first, key.second);
+            if (uploads) uploads->done.emplace_back(key, idx);
+        }
+        idx_ptr = static_cast<const std::uint64_t*>(idx.data());
     }
 
     const void* base = nullptr;
@@ -105,9 +111,7 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
         check(synk_copy(rd->h, staged.data(), src.bytes(), src.byte_size()), "excerpt: stage pageable source");
         base = staged.data();
     }
-    check(synk_gather_rows(rd->h, base, n_src, row_bytes, static_cast<const std::uint64_t*>(idx.data()), part.count(),
-                           out.data()),
-          "gather_rows");
+    check(synk_gather_rows(rd->h, base, n_src, row_bytes, idx_ptr, part.count(), out.data()), "gather_rows");
     return out;
 }
 

@@ -155,6 +155,63 @@ def test_borrowed_and_pinned_index_arrays(sk, oracle):
         assert pool.alive
 
 
+@pytest.mark.parametrize("world", [1, 2])
+def test_device_checked_indexes_raise_bounds_error(sk, world):
+    """Device kernels without updates skip the host scan of the index list: the
+    gather kernel checks every index and call() raises the same BoundsError
+    (same message, pool alive) after the phase. Error order is the reference's:
+    a bad index wins over errors validated after it (function.cpp:266)."""
+    rng = np.random.default_rng(5)
+    src = rng.uniform(-1, 1, (1000, 32)).astype(np.float32)
+    with sk.Pool(workers=world) as pool:
+        arr = sk.SharedInput.from_array(src)
+        arr.mirror(pool)
+        f = sk.make_function(pool, sk.identity_kernel(), ["scatter"], ["gather"])
+        cnt = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
+        sk.distribute(pool)
+        pinned = sk.pinned_array(900, "int64")
+        pinned[:] = rng.integers(0, 1000, 900)
+        pinned[850] = 1000  # only the last rank's share holds the bad index
+        for sel in (pinned, np.asarray(pinned).copy(), np.asarray(pinned).astype(np.uint64)):
+            for fn in (f, cnt):
+                with pytest.raises(sk.BoundsError, match="1000 not within 1000 rows"):
+                    fn.call([arr], indexes=sel)
+                assert pool.alive
+        pinned[850] = 999
+        (got,) = f.call([arr], indexes=pinned)
+        assert got.tobytes() == src[np.asarray(pinned)].tobytes()
+        assert float(cnt.call([arr], indexes=pinned)[0]) == 900.0
+        # error order: BoundsError before the replica_indexes ArgumentError
+        pinned[3] = 5000
+        with pytest.raises(sk.BoundsError):
+            f.call([arr], indexes=pinned, replica_indexes=[(0, 1)])
+        pinned[3] = 3
+        with pytest.raises(sk.ArgumentError):
+            f.call([arr], indexes=pinned, replica_indexes=[(0, 1)])
+
+
+def test_bad_index_with_updates_leaves_variables_untouched(sk):
+    """Kernels with updates keep the host-side check before the phase, so a
+    BoundsError cannot leave a half-applied update behind."""
+    data = np.arange(8.0).reshape(8, 1)
+
+    def total(inputs, ctx):
+        return [np.float64(inputs[0].sum()).reshape(()), inputs[0].sum(axis=0)]
+
+    with sk.Pool(workers=2) as pool:
+        acc = sk.replicate(pool, np.zeros(1))
+        f = sk.make_py_function(pool, "total", total, ["scatter"], ["sum"], updates=[(acc, "add")])
+        sk.distribute(pool)
+        idx = sk.pinned_array(4, "int64")
+        idx[:] = [1, 2, 3, 8]
+        with pytest.raises(sk.BoundsError):
+            f.call([data], indexes=idx)
+        assert acc.get(0)[0] == 0.0 and acc.get(1)[0] == 0.0
+        idx[3] = 7
+        (t,) = f.call([data], indexes=idx)
+        assert t == 13.0 and acc.get(0)[0] == 3.0 and acc.get(1)[0] == 10.0
+
+
 def test_gather_golden_through_api(sk):
     g = golden("gather.npz")
     for tag in ("f32", "f64"):

@@ -85,6 +85,60 @@ def test_gather_from_pinned_host_memory(oracle):
         lib().synk_host_free(host)
 
 
+def _pinned_copy(arr):
+    host = _vp()
+    check(lib().synk_host_alloc(_u64(max(arr.nbytes, 1)), ctypes.byref(host)), "host alloc")
+    ctypes.memmove(host, arr.ctypes.data, arr.nbytes)
+    return host
+
+
+@pytest.mark.parametrize("idx_in", ["hbm", "pinned"])
+def test_gather_wide_rows_bulk_path(oracle, idx_in):
+    """Rows of 4-8 KiB take the cp.async.bulk (TMA engine) kernel; index lists
+    may sit in HBM or in pinned host memory (read in place over PCIe)."""
+    rng = np.random.default_rng(3)
+    with Ranks(1) as R:
+        for dtype, shape in ((np.float32, (3000, 1024)), (np.float64, (500, 1024)), (np.float32, (257, 2048)),
+                             (np.float32, (300, 1028))):
+            src = rng.uniform(-1, 1, shape).astype(dtype)
+            d_src = R.upload(src)
+            for n_idx in (1, 5, 31, 33, 1000, 4099):
+                idx = rng.integers(0, shape[0], n_idx).astype(np.uint64)
+                hidx = _pinned_copy(idx) if idx_in == "pinned" else None
+                d_idx = hidx.value if hidx is not None else R.upload(idx)
+                d_out = R.alloc(n_idx * src[0].nbytes)
+                check(lib().synk_gather_rows(R[0], _vp(d_src), _u64(shape[0]), _u64(src[0].nbytes), _vp(d_idx),
+                                             _u64(n_idx), _vp(d_out)), "gather")
+                check(R.sync(), "sync")
+                if hidx is not None:
+                    lib().synk_host_free(hidx)
+                got = R.download(d_out, (n_idx,) + shape[1:], dtype)
+                assert got.tobytes() == oracle.gather_rows(src, idx).tobytes()
+            bad = np.array([0, 3, shape[0], 1] * 20, np.uint64)
+            d_out = R.alloc(bad.size * src[0].nbytes)
+            check(lib().synk_gather_rows(R[0], _vp(d_src), _u64(shape[0]), _u64(src[0].nbytes), _vp(R.upload(bad)),
+                                         _u64(bad.size), _vp(d_out)), "gather")
+            assert R.sync() == -1  # SYNK_EBOUNDS
+            assert R.sync() == 0
+
+
+def test_gather_index_list_in_pinned_host_memory(oracle):
+    """The 16-byte vector kernel reading its index list over PCIe (e2e path of
+    Function.call with a pinned index array)."""
+    rng = np.random.default_rng(4)
+    src = rng.uniform(-1, 1, (5000, 256)).astype(np.float32)
+    with Ranks(1) as R:
+        d_src = R.upload(src)
+        for n_idx in (1, 4, 5, 4096, 100003):
+            idx = rng.integers(0, 5000, n_idx).astype(np.uint64)
+            hidx = _pinned_copy(idx)
+            d_out = R.alloc(n_idx * 1024)
+            check(lib().synk_gather_rows(R[0], _vp(d_src), _u64(5000), _u64(1024), hidx, _u64(n_idx), _vp(d_out)), "g")
+            check(R.sync(), "sync")
+            lib().synk_host_free(hidx)
+            assert R.download(d_out, (n_idx, 256), np.float32).tobytes() == oracle.gather_rows(src, idx).tobytes()
+
+
 def test_gather_out_of_range_raises_bounds():
     with Ranks(1) as R:
         src = np.zeros((4, 2))
