@@ -31,6 +31,11 @@ namespace synk {
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t err, const char* what);
 
+// Opt a kernel into `bytes` of dynamic shared memory on `device`. The
+// attribute is per-device state (each GPU's context has its own copy of the
+// function), so it is set once per (kernel, device) pair, thread-safely.
+int ensure_max_smem(const void* kernel, int device, int bytes);
+
 #define SYNK_CU(call)                                                   \
     do {                                                                \
         cudaError_t synk_e_ = (call);                                   \

@@ -267,12 +267,8 @@ int launch_bulk(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_by
     uint32_t stages = (uint32_t)(kSmemBudget / (chunk_rows * row_bytes));
     if (stages > kMaxStages) stages = kMaxStages;
     const uint32_t smem = stages * chunk_rows * (uint32_t)row_bytes;
-    static bool attr_set[64] = {};  // per device (the attribute is per-device state)
-    if (d->device >= 64 || !attr_set[d->device]) {
-        SYNK_CU(cudaFuncSetAttribute(gather_rows_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(224u * 1024u)));
-        if (d->device < 64) attr_set[d->device] = true;
-    }
+    if (int rc = synk::ensure_max_smem((const void*)gather_rows_bulk_kernel, d->device, (int)(224u * 1024u)); rc)
+        return rc;
     const uint64_t n_chunks = (n_idx + chunk_rows - 1) / chunk_rows;
     const uint64_t cap = (uint64_t)d->num_sms * ctas_per_sm;
     const unsigned grid = (unsigned)(n_chunks < cap ? n_chunks : cap);

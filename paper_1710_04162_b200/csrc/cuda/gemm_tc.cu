@@ -669,7 +669,6 @@ template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
            uint32_t kb_per = 0x7fffffffu) {
-    static bool attr_set[2][2] = {{false, false}, {false, false}};
     // Epilogue-heavy launches (short K, or the tanh-derivative reading the
     // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
     // the full register budget. SYNK_GEMM_WARPS=4|8 overrides (A/B runs).
@@ -680,17 +679,13 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
     const bool wide = forced ? forced == 8 : (K <= 512 || e.mode == EPI_TANH_GRAD);
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), splits);
     if (wide) {
-        if (!attr_set[KIND][1]) {
-            SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-            attr_set[KIND][1] = true;
-        }
+        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 256>, d->device, (int)kSmemBytes); rc)
+            return rc;
         gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
                                                                        (uint32_t)K, e, kb_per);
     } else {
-        if (!attr_set[KIND][0]) {
-            SYNK_CU(cudaFuncSetAttribute(gemm_tc_kernel<KIND, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-            attr_set[KIND][0] = true;
-        }
+        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 128>, d->device, (int)kSmemBytes); rc)
+            return rc;
         gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
                                                                        (uint32_t)K, e, kb_per);
     }
@@ -889,11 +884,7 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
         CUtensorMap bw;
         if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
         constexpr size_t smem = (size_t)PStages * (PA + PB) + 1024 + 256;
-        static bool attr = false;
-        if (!attr) {
-            SYNK_CU(cudaFuncSetAttribute(gemm_tc_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel, d->device, (int)smem); rc) return rc;
         const uint64_t tiles = ((M + BM - 1) / BM) * ((N + PBN - 1) / PBN);
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
         gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e);

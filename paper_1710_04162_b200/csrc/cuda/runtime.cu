@@ -31,6 +31,17 @@ int cuda_fail(cudaError_t err, const char* what) {
     return fail(code, std::string(what) + ": " + cudaGetErrorString(err));
 }
 
+static std::mutex g_attr_mutex;
+static std::set<std::pair<const void*, int>> g_attr_done;
+
+int ensure_max_smem(const void* kernel, int device, int bytes) {
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    if (g_attr_done.count({kernel, device})) return SYNK_OK;
+    SYNK_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    g_attr_done.insert({kernel, device});
+    return SYNK_OK;
+}
+
 static std::mutex g_pool_mutex;
 static std::set<int> g_pools_configured;
 
@@ -90,6 +101,22 @@ int synk_open(int world, const int* device_ids, synk_dev** out) {
             cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
             if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
             else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        }
+    }
+    // Replicas and per-call buffers come from each device's stream-ordered
+    // pool; peer access to pool memory is granted per pool (peer access
+    // between the devices does not cover it), so every peer of the world may
+    // read and write every device's pool (P2P collectives, rank folds).
+    for (int a : devs) {
+        cudaMemPool_t pool;
+        SYNK_CU(cudaDeviceGetDefaultMemPool(&pool, a));
+        for (int b : devs) {
+            if (a == b) continue;
+            cudaMemAccessDesc desc{};
+            desc.location.type = cudaMemLocationTypeDevice;
+            desc.location.id = b;
+            desc.flags = cudaMemAccessFlagsProtReadWrite;
+            SYNK_CU(cudaMemPoolSetAccess(pool, &desc, 1));
         }
     }
     for (int r = 0; r < world; ++r) {

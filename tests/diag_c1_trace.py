@@ -24,7 +24,12 @@ with sk.Pool(workers=world) as pool:
     g = sk.mlp_grad_function(pool, block)
     sk.distribute(pool)
     tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
-    sel = [rng.integers(0, 65536, 256 * world) for _ in range(400)]
+    def pinned(n):
+        b = sk.pinned_array(n, "int64")
+        b[:] = rng.integers(0, 65536, n)
+        return b
+
+    sel = [pinned(256 * world) for _ in range(400)]
     for s in range(50):
         tr.train_step(g, [sx, sy], indexes=sel[s])
     t0 = time.perf_counter()
