@@ -225,6 +225,20 @@ int synk_gemm_tc(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, co
                  uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int epilogue, int out_dtype,
                  void* c, uint64_t ldc, void* ct, uint64_t ldct, const float* bias, const void* act,
                  uint64_t ldact);
+/* synk_gemm_tc with operand layouts (bf16 only for non-zero bits):
+ * layout bit 0 (SYNK_GEMM_A_MN): A stored MN-major, as K x M with M contiguous
+ *   (leading dim lda) -- e.g. the activation a_l [n x d_l] as A = a_l^T;
+ * layout bit 1 (SYNK_GEMM_B_MN): B stored as K x N with N contiguous (ldb) --
+ *   e.g. W_l [d_l x d_l+1] as the forward product's B = W_l^T.
+ * The tensor cores read MN-major shared-memory tiles directly (UMMA major
+ * bits), so the MLP's weight/activation/delta transposes (mlp.cpp:31-73,
+ * 169-208 use W^T, a^T, delta^T) are never materialised. */
+#define SYNK_GEMM_A_MN 1
+#define SYNK_GEMM_B_MN 2
+int synk_gemm_tc2(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
+                  uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int layout, int epilogue,
+                  int out_dtype, void* c, uint64_t ldc, void* ct, uint64_t ldct, const float* bias,
+                  const void* act, uint64_t ldact);
 
 /* ---- example function: tanh MLP loss + gradient (mlp.cpp:134-218) ---------------- */
 /* dims[0..layers]; params flat [W0 b0 W1 b1 ...]; x [n x dims0]; y [n x dims_L].

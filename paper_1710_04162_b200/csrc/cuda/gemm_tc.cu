@@ -95,6 +95,32 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return d;
 }
 
+// MN-major, 128-byte swizzled operand tile (bf16): TMA boxes of 64 MN
+// elements (128 B) x 64 K rows, one box after another along MN. Canonical
+// SW128 MN-major atom = 64 MN x 8 K rows (1024 B): the next 8 K rows sit 1024 B
+// on (SBO), the next 64 MN elements one box (64 x 128 B) on (LBO).
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((64 * 128) >> 4) << 16;  // leading byte offset: next 64-element MN block
+    d |= (uint64_t)(1024 >> 4) << 32;        // stride byte offset: next 8 K rows
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// Operand layouts (synk_gemm_tc2 `layout` bits): A and/or B stored MN-major
+// (A as K x M, B as K x N, the M / N index contiguous). UMMA reads them as
+// they lie (instruction-descriptor major bits 15 / 16), so no transposed copy
+// of an operand is ever materialised.
+constexpr uint32_t kAMn = 1, kBMn = 2;
+
+// Descriptor of UMMA K-step k (16 bf16) of a stage's operand tile.
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int k, bool mn) {
+    return mn ? smem_desc_mn(base + 2048 * k)  // 16 K rows x 128 B
+              : smem_desc(base + 32 * k);      // 16 elements x 2 B within the swizzled 128-byte row
+}
+
 template <int KIND>  // 0 = kind::f16 (bf16), 1 = kind::tf32
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
     if constexpr (KIND == 0) {
@@ -179,7 +205,7 @@ template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
 __global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
-                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per) {
+                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per, uint32_t layout) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -233,21 +259,32 @@ __global__ void __launch_bounds__(NT, 2)
             const CUtensorMap* mb = pass == 1 ? &b1 : &b0;
             const uint32_t full = smem_u32(&bars[s]);
             mbar_expect_tx(full, 2 * kTileBytes);
-            tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, (kb0 + kb) * kBK, (int)m0);
-            tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, (kb0 + kb) * kBK, (int)n0);
+            const int kc = (kb0 + kb) * kBK;
+            if (layout & kAMn) {  // two 64(M) x 64(K) boxes
+                tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, (int)m0, kc);
+                tma_load_2d(smem_u32(sa + s * kTileBytes + 8192), ma, full, (int)m0 + 64, kc);
+            } else {
+                tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, kc, (int)m0);
+            }
+            if (layout & kBMn) {
+                tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, (int)n0, kc);
+                tma_load_2d(smem_u32(sb + s * kTileBytes + 8192), mb, full, (int)n0 + 64, kc);
+            } else {
+                tma_load_2d(smem_u32(sb + s * kTileBytes), mb, full, kc, (int)n0);
+            }
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
-        constexpr uint32_t idesc = instr_desc<KIND>();
+        const bool amn = layout & kAMn, bmn = layout & kBMn;
+        const uint32_t idesc = instr_desc<KIND>() | (amn ? 1u << 15 : 0u) | (bmn ? 1u << 16 : 0u);
         for (int it = 0; it < total; ++it) {
             const int s = it % kStages;
             mbar_wait(smem_u32(&bars[s]), (it / kStages) & 1);
             tc_fence_after();
             const uint32_t a_base = smem_u32(sa + s * kTileBytes), b_base = smem_u32(sb + s * kTileBytes);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K slices per 128-byte row (UMMA_K = 16 bf16 | 8 tf32)
-                umma<KIND>(tmem, smem_desc(a_base + 32 * k), smem_desc(b_base + 32 * k), idesc,
-                           (it > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {  // 4 K-steps per 64-row stage (UMMA_K = 16 bf16 | 8 tf32)
+                umma<KIND>(tmem, op_desc(a_base, k, amn), op_desc(b_base, k, bmn), idesc, (it > 0 || k > 0) ? 1u : 0u);
             }
             umma_commit(smem_u32(&bars[kStages + s]));  // smem stage free once these MMAs retire
         }
@@ -509,7 +546,7 @@ constexpr int PA = 128 * 128, PB = 256 * 128;  // bytes per stage: A 128 rows, B
 
 __global__ void __launch_bounds__(PThreads, 1)
     gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                              uint32_t M, uint32_t N, uint32_t K, EpiArgs epi) {
+                              uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t layout) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sa = smem;
@@ -559,14 +596,25 @@ __global__ void __launch_bounds__(PThreads, 1)
                 const int s = it % PStages;
                 mbar_wait(smem_u32(&empty[s]), ((it / PStages) & 1) ^ 1);
                 mbar_expect_tx(smem_u32(&full[s]), PA + PB);
-                tma_load_2d(smem_u32(sa + s * PA), &ta, smem_u32(&full[s]), kb * kBK, m0);
-                tma_load_2d(smem_u32(sb + s * PB), &tb, smem_u32(&full[s]), kb * kBK, n0);
+                if (layout & kAMn) {  // 64(M) x 64(K) boxes along M
+                    for (int j = 0; j < BM / 64; ++j)
+                        tma_load_2d(smem_u32(sa + s * PA + j * 8192), &ta, smem_u32(&full[s]), m0 + 64 * j, kb * kBK);
+                } else {
+                    tma_load_2d(smem_u32(sa + s * PA), &ta, smem_u32(&full[s]), kb * kBK, m0);
+                }
+                if (layout & kBMn) {
+                    for (int j = 0; j < PBN / 64; ++j)
+                        tma_load_2d(smem_u32(sb + s * PB + j * 8192), &tb, smem_u32(&full[s]), n0 + 64 * j, kb * kBK);
+                } else {
+                    tma_load_2d(smem_u32(sb + s * PB), &tb, smem_u32(&full[s]), kb * kBK, n0);
+                }
             }
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
-        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PBN >> 3) << 17) |
-                                   ((uint32_t)(BM >> 4) << 24);
+        const bool amn = layout & kAMn, bmn = layout & kBMn;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (amn ? 1u << 15 : 0u) | (bmn ? 1u << 16 : 0u) |
+                               ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
         uint32_t it = 0, tl = 0;
         for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl & 1;
@@ -580,7 +628,7 @@ __global__ void __launch_bounds__(PThreads, 1)
                 const uint32_t a_base = smem_u32(sa + s * PA), b_base = smem_u32(sb + s * PB);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    umma<0>(d, smem_desc(a_base + 32 * k), smem_desc(b_base + 32 * k), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    umma<0>(d, op_desc(a_base, k, amn), op_desc(b_base, k, bmn), idesc, (kb > 0 || k > 0) ? 1u : 0u);
                 umma_commit(smem_u32(&empty[s]));
             }
             umma_commit(smem_u32(&tfull[acc]));
@@ -663,12 +711,30 @@ int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint
     return SYNK_OK;
 }
 
+// MN-major bf16 operand stored as k_rows x mn (mn contiguous, leading
+// dimension ld elements); box = 64 MN elements (128 B) x 64 K rows.
+int make_map_mn(CUtensorMap* map, const void* base, uint64_t k_rows, uint64_t mn, uint64_t ld) {
+    EncodeFn enc = encoder();
+    SYNK_REQUIRE(enc != nullptr, SYNK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    SYNK_REQUIRE(((uintptr_t)base % 16) == 0 && (ld * 2) % 16 == 0, SYNK_EARG,
+                 "gemm_tc: operand base and row pitch must be 16-byte aligned");
+    cuuint64_t dims[2] = {mn, k_rows};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SYNK_REQUIRE(r == CUDA_SUCCESS, SYNK_ECUDA, "cuTensorMapEncodeTiled (MN-major) failed");
+    return SYNK_OK;
+}
+
 constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
-           uint32_t kb_per = 0x7fffffffu) {
+           uint32_t kb_per = 0x7fffffffu, uint32_t layout = 0) {
     // Epilogue-heavy launches (short K, or the tanh-derivative reading the
     // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
     // the full register budget. SYNK_GEMM_WARPS=4|8 overrides (A/B runs).
@@ -682,12 +748,12 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 256>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per);
+                                                                       (uint32_t)K, e, kb_per, layout);
     } else {
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 128>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per);
+                                                                       (uint32_t)K, e, kb_per, layout);
     }
     SYNK_LAUNCHED("gemm_tc_kernel");
     return SYNK_OK;
@@ -854,15 +920,26 @@ int synk_gemm_prep(synk_dev* d, int in_dtype, const void* in, uint64_t rows, uin
 int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
                  uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int epilogue, int out_dtype, void* c,
                  uint64_t ldc, void* ct, uint64_t ldct, const float* bias, const void* act, uint64_t ldact) {
+    return synk_gemm_tc2(d, kind, M, N, K, a_hi, a_lo, lda, b_hi, b_lo, ldb, 0, epilogue, out_dtype, c, ldc, ct, ldct,
+                         bias, act, ldact);
+}
+
+int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
+                  uint64_t lda, const void* b_hi, const void* b_lo, uint64_t ldb, int layout, int epilogue,
+                  int out_dtype, void* c, uint64_t ldc, void* ct, uint64_t ldct, const float* bias, const void* act,
+                  uint64_t ldact) {
     SYNK_REQUIRE(kind >= 0 && kind <= 2, SYNK_EARG, "gemm_tc: kind is 0 (bf16), 1 (tf32) or 2 (3xtf32)");
+    SYNK_REQUIRE(layout >= 0 && layout <= 3 && (layout == 0 || kind == 0), SYNK_EARG,
+                 "gemm_tc: MN-major operands (layout bits) are bf16 only");
     SYNK_REQUIRE(out_dtype == SYNK_F32 || out_dtype == 3, SYNK_EDTYPE, "gemm_tc: output f32 or bf16");
     SYNK_REQUIRE(M < (1ull << 31) && N < (1ull << 31) && K < (1ull << 31), SYNK_EARG, "gemm_tc: dims too large");
     if (M == 0 || N == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     const bool bf16 = kind == 0;
+    const uint32_t lay = (uint32_t)layout;
     CUtensorMap a0, a1, b0, b1;
-    if (int rc = make_map(&a0, a_hi, M, K, lda, bf16); rc) return rc;
-    if (int rc = make_map(&b0, b_hi, N, K, ldb, bf16); rc) return rc;
+    if (int rc = (lay & kAMn) ? make_map_mn(&a0, a_hi, K, M, lda) : make_map(&a0, a_hi, M, K, lda, bf16); rc) return rc;
+    if (int rc = (lay & kBMn) ? make_map_mn(&b0, b_hi, K, N, ldb) : make_map(&b0, b_hi, N, K, ldb, bf16); rc) return rc;
     a1 = a0;
     b1 = b0;
     if (kind == 2) {
@@ -881,13 +958,15 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
         return v ? atoi(v) : 1;
     }();
     if (bf16 && persistent_mode && N > 128) {
-        CUtensorMap bw;
-        if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
+        CUtensorMap bw = b0;
+        if (!(lay & kBMn))
+            if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
         constexpr size_t smem = (size_t)PStages * (PA + PB) + 1024 + 256;
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel, d->device, (int)smem); rc) return rc;
         const uint64_t tiles = ((M + BM - 1) / BM) * ((N + PBN - 1) / PBN);
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
-        gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e);
+        gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e,
+                                                                         lay);
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
         return SYNK_OK;
     }
@@ -910,7 +989,7 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
         float* planes = nullptr;
         SYNK_CU(cudaMallocAsync((void**)&planes, (size_t)splits * M * N * sizeof(float), d->stream));
         EpiArgs pe{SYNK_EPI_STORE, 0, planes, N, nullptr, 0, nullptr, nullptr, 0};
-        int rc = bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per)
+        int rc = bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per, lay)
                       : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per);
         if (rc) return rc;
         const unsigned fgrid = (unsigned)std::min<uint64_t>((M * N + 255) / 256, (uint64_t)d->num_sms * 8);
@@ -920,7 +999,7 @@ int synk_gemm_tc(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, cons
         SYNK_CU(cudaFreeAsync(planes, d->stream));
         return SYNK_OK;
     }
-    return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e)
+    return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e, 1, 0x7fffffffu, lay)
                 : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, e);
 }
 

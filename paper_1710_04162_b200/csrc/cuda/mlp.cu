@@ -341,13 +341,25 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
 }
 
 // ---- bf16 tensor-core path (config C5: wide MLP, fp32 master weights) -----------------
-// Every dense product is one synk_gemm_tc (tcgen05 kind::f16) launch with all
-// operands K-major: the forward epilogue writes each hidden activation both
-// row-major (next layer's A) and transposed (its weight gradient's A), the dX
-// epilogue does the same for delta, so no separate transpose kernel touches
-// activations. Weights are cast/transposed to bf16 once per step.
+// Every dense product is one synk_gemm_tc2 (tcgen05 kind::f16) launch. Operand
+// layouts follow what the tensor cores read at full speed (measured,
+// profiles/r01_gemm_layouts.txt): B may be MN-major for free on the 128x256
+// persistent path (N > 128), while an MN-major A costs 10-20 % and an MN-major
+// B on the narrow (N <= 128) path ~30 %. Hence:
+//   forward   a_{l+1} = tanh(a_l . W_l + b_l): A = a_l (K-major); B = W_l as it
+//             lies (MN-major) when d_{l+1} > 128, else W_l^T (a small cast +
+//             transpose); the epilogue stores a_{l+1} and a_{l+1}^T;
+//   gradient  [gW_l; gb_l] = [a_l^T; 1] . delta: A = a_l^T (K-major, its extra
+//             row of ones yields the bias gradient); B = delta MN-major when
+//             d_{l+1} > 128, else delta^T (emitted by the producer of delta);
+//   dX        delta_prev = (delta . W_l^T) * (1 - a_l^2): A = delta, B = W_l,
+//             both K-major as they lie.
+// So the only transposes are a_l^T (epilogue stores; x^T by the cast) and
+// the narrow output layer's W^T / delta^T.
 
 inline uint64_t pad8(uint64_t v) { return (v + 7) / 8 * 8; }
+
+constexpr uint64_t kWideN = 128;  // N > kWideN: persistent path, MN-major B at full speed
 
 // Row `row` of each a_l^T buffer = 1.0 (bf16), so the weight-gradient GEMM
 // over M = d_l + 1 rows also yields sum_i delta[i, :] = the bias gradient,
@@ -366,7 +378,7 @@ __global__ void __launch_bounds__(256) ones_rows_kernel(OnesRows rows, uint64_t 
 struct Bf16Plan {
     uint64_t n, maxd, L;
     uint64_t off_w[64], off_wt[64], off_act[65], off_actT[65];
-    uint64_t off_pred, off_delta_f, off_d[2], off_dT[2], off_partial, total;
+    uint64_t off_pred, off_delta_f, off_d[2], off_dT, off_partial, total;
 };
 
 Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t maxd) {
@@ -380,9 +392,13 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
         at += (bytes + 255) / 256 * 256;
         return o;
     };
+    uint64_t narrow = 0;  // widest output dimension <= kWideN (needs W^T and delta^T)
     for (uint32_t l = 0; l < L; ++l) {
         p.off_w[l] = take(dims[l] * pad8(dims[l + 1]) * 2);
-        p.off_wt[l] = take(dims[l + 1] * pad8(dims[l]) * 2);
+        if (dims[l + 1] <= kWideN) {
+            p.off_wt[l] = take(dims[l + 1] * pad8(dims[l]) * 2);
+            narrow = std::max<uint64_t>(narrow, dims[l + 1]);
+        }
     }
     for (uint32_t l = 0; l < L; ++l) {  // act[0] = x, act[l] hidden
         p.off_act[l] = take(n * pad8(dims[l]) * 2);
@@ -390,10 +406,8 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
     }
     p.off_pred = take(n * dims[L] * 4);
     p.off_delta_f = take(n * dims[L] * 4);
-    for (int i = 0; i < 2; ++i) {
-        p.off_d[i] = take(n * pad8(maxd) * 2);
-        p.off_dT[i] = take(maxd * pad8(n) * 2);
-    }
+    for (int i = 0; i < 2; ++i) p.off_d[i] = take(n * pad8(maxd) * 2);
+    p.off_dT = take(std::max<uint64_t>(narrow, 1) * pad8(n) * 2);
     p.off_partial = take(kLossBlocks * sizeof(double));
     p.total = at;
     return p;
@@ -405,12 +419,13 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     char* base = static_cast<char*>(ws);
     auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
     const int F32 = SYNK_F32, BF = SYNK_BF16;
+    auto wide = [&](uint32_t l) { return dims[l + 1] > kWideN; };  // output width of layer l
 
-    // weights: W_l (K-major for dX) and W_l^T (K-major for the forward), one read each
+    // weights: W_l in bf16 (+ W_l^T for narrow layers), one read each
     for (uint32_t l = 0; l < L; ++l) {
         const float* W = theta + P.woff[l];
         if (int rc = synk_gemm_prep2_bf16(d, W, dims[l], dims[l + 1], dims[l + 1], bf(B.off_w[l]), pad8(dims[l + 1]),
-                                          bf(B.off_wt[l]), pad8(dims[l]));
+                                          wide(l) ? nullptr : bf(B.off_wt[l]), pad8(dims[l]));
             rc)
             return rc;
     }
@@ -419,7 +434,6 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
                                       pad8(n));
         rc)
         return rc;
-
     {
         OnesRows o{};
         o.count = L;
@@ -432,15 +446,17 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     float* pred = reinterpret_cast<float*>(base + B.off_pred);
     for (uint32_t l = 0; l < L; ++l) {
         const bool hidden = l + 1 < L;
-        int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, n, dims[l + 1], dims[l], bf(B.off_act[l]), nullptr, pad8(dims[l]),
-                              bf(B.off_wt[l]), nullptr, pad8(dims[l]), hidden ? SYNK_EPI_BIAS_TANH : SYNK_EPI_BIAS,
-                              hidden ? BF : F32, hidden ? (void*)bf(B.off_act[l + 1]) : (void*)pred,
-                              hidden ? pad8(dims[l + 1]) : dims[L], hidden ? (void*)bf(B.off_actT[l + 1]) : nullptr,
-                              pad8(n), theta + P.boff[l], nullptr, 0);
+        const void* b = wide(l) ? (const void*)bf(B.off_w[l]) : (const void*)bf(B.off_wt[l]);
+        const uint64_t ldb = wide(l) ? pad8(dims[l + 1]) : pad8(dims[l]);
+        int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, dims[l + 1], dims[l], bf(B.off_act[l]), nullptr, pad8(dims[l]), b,
+                               nullptr, ldb, wide(l) ? SYNK_GEMM_B_MN : 0, hidden ? SYNK_EPI_BIAS_TANH : SYNK_EPI_BIAS,
+                               hidden ? BF : F32, hidden ? (void*)bf(B.off_act[l + 1]) : (void*)pred,
+                               hidden ? pad8(dims[l + 1]) : dims[L], hidden ? (void*)bf(B.off_actT[l + 1]) : nullptr,
+                               pad8(n), theta + P.boff[l], nullptr, 0);
         if (rc) return rc;
     }
 
-    // loss + output delta (f32), then its bf16 operand forms
+    // loss + output delta (f32), then its bf16 operand form(s)
     const uint64_t dl = dims[L], n_el = n * dl;
     float* delta_f = reinterpret_cast<float*>(base + B.off_delta_f);
     double* partial = reinterpret_cast<double*>(base + B.off_partial);
@@ -451,7 +467,8 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     loss_final_kernel<<<1, 256, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
     SYNK_LAUNCHED("loss_final_kernel");
     int cur = 0;
-    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd), bf(B.off_dT[cur]), pad8(n));
+    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd),
+                                      wide(L - 1) ? nullptr : bf(B.off_dT), pad8(n));
         rc)
         return rc;
 
@@ -459,17 +476,20 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     for (uint32_t l = L; l-- > 0;) {
         const uint64_t din = dims[l], dout = dims[l + 1];
         // [gW_l; gb_l] = [a_l^T; 1] . delta  (M = din + 1: the last row is the bias gradient)
-        if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, din + 1, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), bf(B.off_dT[cur]),
-                                  nullptr, pad8(n), SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr,
-                                  nullptr, 0);
+        const void* b = wide(l) ? (const void*)bf(B.off_d[cur]) : (const void*)bf(B.off_dT);
+        if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, din + 1, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), b,
+                                   nullptr, wide(l) ? pad8(P.maxd) : pad8(n), wide(l) ? SYNK_GEMM_B_MN : 0,
+                                   SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr, nullptr, 0);
             rc)
             return rc;
         if (l > 0) {
             // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
             const int nxt = cur ^ 1;
-            if (int rc = synk_gemm_tc(d, SYNK_GEMM_BF16, n, din, dout, bf(B.off_d[cur]), nullptr, pad8(P.maxd),
-                                      bf(B.off_w[l]), nullptr, pad8(dout), SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
-                                      pad8(P.maxd), bf(B.off_dT[nxt]), pad8(n), nullptr, bf(B.off_act[l]), pad8(din));
+            const bool narrow_prev = !wide(l - 1);  // gW_{l-1} then wants delta_prev^T
+            if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, din, dout, bf(B.off_d[cur]), nullptr, pad8(P.maxd),
+                                       bf(B.off_w[l]), nullptr, pad8(dout), 0, SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
+                                       pad8(P.maxd), narrow_prev ? (void*)bf(B.off_dT) : nullptr, pad8(n), nullptr,
+                                       bf(B.off_act[l]), pad8(din));
                 rc)
                 return rc;
             cur = nxt;

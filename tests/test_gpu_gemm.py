@@ -190,3 +190,66 @@ def test_prep2_bf16_cast_and_transpose(rows, cols):
         got_t = R.download(ot, (cols, ldt), np.uint16)[:, :rows]
     np.testing.assert_array_equal(got, want.astype(np.uint16))
     np.testing.assert_array_equal(got_t, want.T.astype(np.uint16))
+
+
+def gemm_layout(R, a, b, layout, epi="store", bias=None, act=None, out_bf16=False):
+    """bf16 C = epi(a @ b.T) with A stored MN-major (as a.T, K x M) when
+    layout & 1 and B stored MN-major (as b.T, K x N) when layout & 2."""
+    M, K = a.shape
+    N = b.shape[0]
+    ahi, _, lda = prep(R, a.T if layout & 1 else a, False, 1)
+    bhi, _, ldb = prep(R, b.T if layout & 2 else b, False, 1)
+    es = 2 if out_bf16 else 4
+    c = R.alloc(M * N * es)
+    dbias = R.upload(bias.astype(np.float32)) if bias is not None else 0
+    dact = 0
+    if act is not None:
+        dact = R.alloc(M * N * 2)
+        da = R.upload(act.astype(np.float32))
+        check(lib().synk_gemm_prep(R[0], F32, _vp(da), _u64(M), _u64(N), _u64(N), 0, 1, _vp(dact), None, _u64(M),
+                                   _u64(N), _u64(N)), "prep act")
+    check(lib().synk_gemm_tc2(R[0], 0, _u64(M), _u64(N), _u64(K), _vp(ahi), None, _u64(lda), _vp(bhi), None, _u64(ldb),
+                              layout, EPI[epi], BF16 if out_bf16 else F32, _vp(c), _u64(N), None, _u64(0),
+                              _vp(dbias or None), _vp(dact or None), _u64(N)), "gemm_tc2")
+    check(R.sync(), "sync")
+    if out_bf16:
+        raw = R.download(c, (M, N), np.uint16).astype(np.uint32) << 16
+        return raw.view(np.float32)
+    return R.download(c, (M, N), np.float32)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 200, 100), (129, 520, 72), (4096, 2048, 512),
+                                   (4097, 100, 8192), (8192, 100, 4096), (1000, 4000, 600)])
+@pytest.mark.parametrize("layout", [1, 2, 3])
+def test_bf16_mn_major_operands(M, N, K, layout):
+    """MN-major A and/or B (UMMA major bits, 64x64 TMA boxes): bitwise equal
+    to the K-major product of the same bf16 operands, on the persistent
+    128x256 path, the 128x128 path and the split-K path; and within the
+    fp32-accumulation bound of the fp64 product."""
+    rng = np.random.default_rng(M * 3 + N + K + layout)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)))
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        ref = gemm_layout(R, a, b, 0)
+        got = gemm_layout(R, a, b, layout)
+    assert rel_err(got, want) <= 1e-6 + 5e-8 * K
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_bf16_mn_major_fused_epilogues():
+    """The MLP's forward (B = W MN-major, bias + tanh, bf16 out) and weight-
+    gradient (A = activations, B = delta, both MN-major) products."""
+    rng = np.random.default_rng(9)
+    M, N, K = 512, 384, 256
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)) * 0.1)
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    z = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        for layout in (0, 2, 3):
+            got = gemm_layout(R, a, b, layout, "bias_tanh", bias=bias, out_bf16=True)
+            assert rel_err(got, np.tanh(z + bias)) <= 2.0 ** -7
+            act = bf16_round(np.tanh(rng.uniform(-1, 1, (M, N))))
+            got = gemm_layout(R, a, b, layout, "tanh_grad", act=act, out_bf16=True)
+            assert rel_err(got, z * (1 - act.astype(np.float64) ** 2)) <= 2.0 ** -7 * 4
