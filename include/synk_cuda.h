@@ -88,6 +88,14 @@ int synk_sync(synk_dev* dev);
  * synk_mark_reset recycles every mark of the rank. */
 int synk_mark(synk_dev* dev, int* mark);
 int synk_mark_elapsed(synk_dev* dev, int a, int b, double* seconds);
+
+/* Device-side ordering between ranks without a host barrier: synk_signal
+ * marks the current tail of dev's stream; synk_wait_peer makes dev's stream
+ * wait (on the GPU) until peer's last signalled point has executed. Used to
+ * chain the gradient all-reduce + update onto the gradient phase (the host
+ * phase barrier between sgd.cpp:301 and :314 of the reference). */
+int synk_signal(synk_dev* dev);
+int synk_wait_peer(synk_dev* dev, const synk_dev* peer);
 int synk_mark_reset(synk_dev* dev);
 
 /* ---- memory ------------------------------------------------------------------ */

@@ -148,6 +148,15 @@ private:
     std::variant<NdBuffer, SharedInputArray, ReplicatedVariable> value_;
 };
 
+class ParallelFunction;
+namespace detail {
+struct PhaseRendezvous;
+// Executor internal (the fused trainer step): call() plus work chained inside its phase.
+CallResult call_with_tail(const ParallelFunction& f, const std::vector<FunctionArg>& args, const CallOptions& opts,
+                          const std::function<void(std::size_t, const std::vector<std::size_t>&)>& tail,
+                          PhaseRendezvous* rv);
+} // namespace detail
+
 class ParallelFunction {
 public:
     ParallelFunction() = default;
@@ -167,6 +176,10 @@ private:
     friend ParallelFunction function(WorkerPool&, Kernel, std::vector<InputSpec>, std::vector<OutputSpec>,
                                      std::vector<UpdateSpec>);
     friend void distribute(WorkerPool&);
+    friend CallResult detail::call_with_tail(const ParallelFunction&, const std::vector<FunctionArg>&,
+                                             const CallOptions&,
+                                             const std::function<void(std::size_t, const std::vector<std::size_t>&)>&,
+                                             detail::PhaseRendezvous*);
     explicit ParallelFunction(std::shared_ptr<detail::FunctionCore> core) : core_(std::move(core)) {}
     std::shared_ptr<detail::FunctionCore> core_;
 };

@@ -23,6 +23,7 @@ struct synk_dev {
     volatile int* err_host = nullptr;
     int* err_dev = nullptr;
     std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
+    cudaEvent_t ready = nullptr;     // synk_signal point (no timing), waited on by peers' streams
     int marks_used = 0;
 };
 

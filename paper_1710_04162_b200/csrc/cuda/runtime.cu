@@ -149,6 +149,7 @@ int synk_close(synk_dev* d) {
     cudaFreeHost(d->flags_host);
     cudaFreeHost(const_cast<int*>(d->err_host));
     for (cudaEvent_t e : d->marks) cudaEventDestroy(e);
+    if (d->ready) cudaEventDestroy(d->ready);
     delete d;
     return SYNK_OK;
 }
@@ -181,6 +182,20 @@ int synk_mark(synk_dev* d, int* mark) {
     }
     *mark = d->marks_used++;
     SYNK_CU(cudaEventRecord(d->marks[*mark], d->stream));
+    return SYNK_OK;
+}
+
+int synk_signal(synk_dev* d) {
+    DeviceGuard g(d->device);
+    if (!d->ready) SYNK_CU(cudaEventCreateWithFlags(&d->ready, cudaEventDisableTiming));
+    SYNK_CU(cudaEventRecord(d->ready, d->stream));
+    return SYNK_OK;
+}
+
+int synk_wait_peer(synk_dev* d, const synk_dev* peer) {
+    SYNK_REQUIRE(peer && peer->ready, SYNK_EARG, "synk_wait_peer: the peer has not signalled");
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaStreamWaitEvent(d->stream, peer->ready, 0));
     return SYNK_OK;
 }
 

@@ -12,6 +12,7 @@
 
 #include "synk_cuda.h"
 #include "synkpar/device.hpp"
+#include "synkpar/function.hpp"
 #include "synkpar/worker_pool.hpp"
 
 namespace synkpar::detail {
@@ -105,6 +106,23 @@ struct PoolState {
 };
 
 PhaseReport run_pool_phase(PoolState& st, PhaseKind kind, const std::function<void(std::size_t)>& work);
+
+// Host rendezvous of all rank tasks inside ONE phase (device ordering between
+// ranks then goes through synk_signal / synk_wait_peer, not a stream sync).
+// A rank task that fails before arriving aborts it, so no peer waits forever.
+struct PhaseRendezvous {
+    explicit PhaseRendezvous(std::size_t world) : world(world) {}
+    void arrive_and_wait();  // throws PhaseError-able ArgumentError if aborted
+    void abort() { broken.store(true); }
+    const std::size_t world;
+    std::atomic<std::size_t> arrived{0};
+    std::atomic<bool> broken{false};
+};
+
+// call_with_tail (declared in synkpar/function.hpp): ParallelFunction::call,
+// with tail(rank, eff_rows) run on each rank's thread inside the call's
+// phase, after the rank's share (outputs, updates) is enqueued and before the
+// phase-exit synchronisation. A failing rank task aborts `rv` (if given).
 void shutdown_pool(PoolState& st);
 void require_idle(const PoolState& st, const char* what);
 

@@ -175,6 +175,100 @@ SyncSgd::SyncSgd(WorkerPool& pool, FlatParamBlock block, UpdateRule rule, double
     distribute(pool);
 }
 
+// The all-reduce + update chained onto the gradient call's own phase: each
+// rank enqueues its gradient work, then (W > 1) signals, meets its peers on
+// the host and makes its stream wait for theirs on the device, then enqueues
+// the fused all-reduce + 1/W + update kernel; the phase-exit synchronisation
+// covers both. Same arithmetic, same order as the two-phase path (sgd.cpp:
+// 292-319 of the reference), without the host round trip between them.
+double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<FunctionArg>& batch,
+                           const CallOptions& call_opts, Clock::time_point t0) {
+    StepReport rep;
+    auto st = detail::state_of(*pool_);
+    const std::size_t W = st->world;
+    auto& grads = detail::replicas_of(block_.grads);
+    auto& params = detail::replicas_of(block_.params);
+    for (std::size_t r = 1; r < W; ++r)
+        if (!grads[r].same_shape(grads[0]))
+            throw ShapeError("all_reduce: replica shapes differ across ranks (" + grads[0].shape_string() + " vs rank " +
+                             std::to_string(r) + " " + grads[r].shape_string() + ")");
+    for (std::size_t r = 0; r < W; ++r) {
+        if (params[r].dtype() != grads[r].dtype()) throw DTypeError("step: params/grads dtype mismatch");
+        if (params[r].size() != grads[r].size()) throw ShapeError("step: params length != grads length");
+    }
+    std::vector<void*> pp, a0, a1;
+    for (std::size_t r = 0; r < W; ++r) {
+        pp.push_back(params[r].data());
+        if (aux_.size() > 0) a0.push_back(detail::replicas_of(aux_[0])[r].data());
+        if (aux_.size() > 1) a1.push_back(detail::replicas_of(aux_[1])[r].data());
+    }
+    bool coherent = detail::record_of(block_.params).coherent;
+    for (const ReplicatedVariable& a : aux_) coherent = coherent && detail::record_of(a).coherent;
+    const std::vector<double> hyper = rule_hyper(rule_);
+    const int code = rule_code(rule_);
+    const std::uint64_t t_next = t_ + 1;
+    const bool timing = call_opts.device_timing;
+    int ma = -1, mb = -1;
+    detail::PhaseRendezvous rv(W);
+
+    auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows) {
+        const auto& rd = st->ranks[r];
+        const int dt = detail::synk_dtype(grads[r].dtype());
+        if (opts_.grad_op == ReduceOp::Mean && W > 1) {
+            // Unequal shards: pre-scale each rank's shard-mean gradient by
+            // rows_r*W/total so the equal-weight mean is the global row mean.
+            std::size_t total = 0;
+            bool unequal = false;
+            for (std::size_t x : rows) total += x;
+            for (std::size_t x : rows) unequal |= x * W != total;
+            if (unequal && total > 0)
+                detail::check(synk_scale(rd->h, dt, grads[r].data(), double(rows[r]) * double(W) / double(total),
+                                         grads[r].size()),
+                              "unequal-shard pre-scale");
+        }
+        if (W > 1) {
+            detail::check(synk_signal(rd->h), "signal");
+            rv.arrive_and_wait();
+            for (std::size_t p = 0; p < W; ++p)
+                if (p != r) detail::check(synk_wait_peer(rd->h, st->handles[p]), "wait peer");
+        }
+        // The gradient update may have swapped each rank's grads replica for a
+        // fresh buffer (WeightedMeanByRows adopts its accumulator): read the
+        // pointers only now, after every rank applied its update.
+        std::vector<void*> gp(W);
+        for (std::size_t p = 0; p < W; ++p) gp[p] = grads[p].data();
+        if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
+        detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
+                                           hyper.data(), lr_, t_next, pp.data(), gp.data(),
+                                           a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
+                                           grads[r].size(), coherent ? 1 : 0),
+                      "fused all-reduce + update");
+        if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
+    };
+    CallResult gr = detail::call_with_tail(f_grad, batch, call_opts, tail, &rv);
+    if (gr.outputs.empty()) throw ArgumentError("train_step(): gradient function must output the loss");
+    const double loss = gr.outputs[0].get(0);
+    rep.grad_call = gr.report;
+    if (ma >= 0 && mb >= 0) {
+        double sec = 0.0;
+        detail::check(synk_mark_elapsed(st->ranks[0]->h, ma, mb, &sec), "timing");
+        rep.allreduce_s = sec;
+        rep.step_call.total_s = sec;
+    }
+    rep.step_call.rank_rows.assign(W, 1);
+    detail::record_of(block_.grads).coherent = true;
+    detail::record_of(block_.params).coherent = true;
+    for (const ReplicatedVariable& a : aux_) detail::record_of(a).coherent = true;
+    t_ += 1;
+    if (opts_.verify_coherence && !block_.params.replicas_coherent())
+        throw CoherenceError("train_step(): parameter replicas diverged after step " + std::to_string(t_));
+    rep.loss = loss;
+    rep.total_s = since(t0);
+    last_ = rep;
+    return loss;
+}
+
+
 double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<FunctionArg>& batch,
                            const CallOptions& call_opts) {
     const auto t0 = Clock::now();
@@ -189,6 +283,9 @@ double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<Fun
         // Accumulating gradient functions start from zero every step.
         for (std::size_t r = 0; r < W; ++r) block_.grads.set_value(r, NdBuffer::zeros({block_.length}, block_.grads.dtype()));
     }
+
+    if (opts_.all_reduce && !opts_.check_finite && opts_.grad_op != ReduceOp::Gather)
+        return fused_step(f_grad, batch, call_opts, t0);
 
     CallResult gr = f_grad.call(batch, call_opts);
     if (gr.outputs.empty()) throw ArgumentError("train_step(): gradient function must output the loss");
