@@ -327,6 +327,45 @@ def test_kernel_contract_violation_fail_stop(sk):
         assert pool.alive
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_step_rank_failure_fail_stop(sk, world):
+    """The trainer chains the all-reduce + update into the gradient call's
+    phase behind an in-phase rank rendezvous: a rank whose gradient kernel
+    fails must abort it (PhaseError + fail-stop, as the reference), never
+    leave its peers waiting."""
+    params = np.zeros(3)
+
+    def grad(inputs, ctx):
+        if ctx.rank == world - 1:
+            raise RuntimeError("injected gradient failure")
+        return [np.float64(inputs[0].sum()).reshape(()), np.full(3, 1.0)]
+
+    with sk.Pool(workers=world) as pool:
+        block = sk.ParamBlock.create(pool, [params])
+        f = sk.make_py_function(pool, "grad", grad, ["scatter"], ["mean"], updates=[(block.grads, "weighted_mean")])
+        sk.distribute(pool)
+        trainer = sk.Trainer(pool, block, sk.SgdRule(), lr=0.1)
+        with pytest.raises(sk.PhaseError):
+            trainer.train_step(f, [np.arange(12.0).reshape(12, 1)])
+        assert not pool.alive
+
+
+def test_fused_step_python_grad_kernel(sk):
+    """A host (Python) gradient kernel through the fused step: mean of the
+    per-rank gradients, one SGD update, replicas coherent."""
+    def grad(inputs, ctx):
+        return [np.float64(inputs[0].sum()).reshape(()), np.full(2, float(ctx.rank + 1))]
+
+    with sk.Pool(workers=2) as pool:
+        block = sk.ParamBlock.create(pool, [np.array([1.0, 2.0])])
+        f = sk.make_py_function(pool, "grad", grad, ["scatter"], ["mean"], updates=[(block.grads, "weighted_mean")])
+        sk.distribute(pool)
+        trainer = sk.Trainer(pool, block, sk.SgdRule(), lr=0.1, verify_coherence=True)
+        trainer.train_step(f, [np.arange(8.0).reshape(8, 1)])
+        np.testing.assert_allclose(block.params.get(0), np.array([1.0, 2.0]) - 0.1 * 1.5, rtol=1e-15)
+        np.testing.assert_array_equal(block.params.get(1), block.params.get(0))
+
+
 def test_overwrite_and_slicing_conflict(sk):
     with sk.Pool(workers=2) as pool:
         v = sk.replicate(pool, np.zeros(1))
