@@ -15,7 +15,8 @@ struct synk_dev {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
-    int* flags_dev = nullptr;   // [1] scratch result of synchronous checks
+    int* flags_dev = nullptr;   // [1] scratch result of synchronous checks; [3] MLP loss-fold arrival
+                                //     counter (zero between launches: the folding CTA resets it)
     int* flags_host = nullptr;  // pinned mirror for synchronous checks
     // Sticky device-detected error flag (gather bounds), in mapped pinned host
     // memory: kernels write it only on error, synk_sync reads it after the

@@ -25,13 +25,16 @@ constexpr int BM = 64, BN = 64, BK = 16, kThreads = 256;
 enum Epi { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_TANH = 2, EPI_TANH_GRAD = 3 };
 
 // C[m,n] = epi( sum_k A(m,k) B(k,n) ), A(m,k) = A[m*am + k*ak], B(k,n) = B[k*bk + n*bn]
+// Row `ones_row` of A (if < M) reads as 1: the weight-gradient product over
+// M = d_l + 1 rows then also yields the bias gradient (colsum of delta) in
+// its last row, which lands on b_l right after W_l in the flat layout.
 // Split-K (gridDim.z > 1): CTA z sums k in [z*kper, (z+1)*kper) and stores the
 // raw partial to C + z*M*N (ldc = N); splitk_reduce_kernel folds the partials.
 template <class T>
 __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
     int epi, int64_t M, int64_t N, int64_t K, const T* __restrict__ A, int64_t am, int64_t ak,
     const T* __restrict__ B, int64_t bk, int64_t bn, T* __restrict__ C, int64_t ldc,
-    const T* __restrict__ bias, const T* __restrict__ act, int64_t kper) {
+    const T* __restrict__ bias, const T* __restrict__ act, int64_t kper, int64_t ones_row) {
     __shared__ T As[BK][BM + 1];
     __shared__ T Bs[BK][BN + 1];
     const int tid = threadIdx.x;
@@ -57,7 +60,7 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
             if (ak == 1) { kk = idx % BK; mm = idx / BK; }   // K contiguous in memory
             else { mm = idx % BM; kk = idx / BM; }
             int64_t gm = m0 + mm, gk = k0 + kk;
-            As[kk][mm] = (gm < M && gk < kend) ? A[gm * am + gk * ak] : T(0);
+            As[kk][mm] = (gm < M && gk < kend) ? (gm == ones_row ? T(1) : A[gm * am + gk * ak]) : T(0);
             int nn;
             if (bn == 1) { nn = idx % BN; kk = idx / BN; }   // N contiguous in memory
             else { kk = idx % BK; nn = idx / BK; }
@@ -145,20 +148,21 @@ __global__ void __launch_bounds__(kThreads) splitk_reduce_kernel(
 
 template <class T>
 int gemm(synk_dev* d, int epi, int64_t M, int64_t N, int64_t K, const T* A, int64_t am, int64_t ak,
-         const T* B, int64_t bk, int64_t bn, T* C, int64_t ldc, const T* bias, const T* act, T* partials) {
+         const T* B, int64_t bk, int64_t bn, T* C, int64_t ldc, const T* bias, const T* act, T* partials,
+         int64_t ones_row = -1) {
     if (M == 0 || N == 0) return SYNK_OK;
     int64_t kper = 0;
     const int64_t S = split_k(sizeof(T), M, N, K, &kper);
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)S);
     if (S == 1) {
         gemm_simt_kernel<T><<<grid, kThreads, 0, d->stream>>>(epi, M, N, K, A, am, ak, B, bk, bn, C, ldc, bias,
-                                                              act, K > 0 ? K : 1);
+                                                              act, K > 0 ? K : 1, ones_row);
         SYNK_LAUNCHED("gemm_simt_kernel");
         return SYNK_OK;
     }
     SYNK_REQUIRE(partials != nullptr, SYNK_EARG, "mlp gemm: split-K needs a partials workspace");
     gemm_simt_kernel<T><<<grid, kThreads, 0, d->stream>>>(epi, M, N, K, A, am, ak, B, bk, bn, partials, N,
-                                                          nullptr, nullptr, kper);
+                                                          nullptr, nullptr, kper, ones_row);
     SYNK_LAUNCHED("gemm_simt_kernel");
     unsigned rgrid = (unsigned)std::min<int64_t>((M * N + kThreads - 1) / kThreads, 148 * 4);
     splitk_reduce_kernel<T><<<rgrid, kThreads, 0, d->stream>>>(epi, S, M, N, partials, C, ldc, bias, act);
@@ -176,19 +180,25 @@ uint64_t splitk_elems(int es, const uint64_t* dims, uint32_t layers, uint64_t n)
     };
     for (uint32_t l = 0; l < layers; ++l) {
         see((int64_t)n, (int64_t)dims[l + 1], (int64_t)dims[l]);
-        see((int64_t)dims[l], (int64_t)dims[l + 1], (int64_t)n);
+        see((int64_t)dims[l] + 1, (int64_t)dims[l + 1], (int64_t)n);
         if (l > 0) see((int64_t)n, (int64_t)dims[l], (int64_t)dims[l + 1]);
     }
     return best;
 }
 
 // delta = (pred - y) * inv_n ; per-CTA partial of sum (pred - y)^2 in f64.
+// With `counter`, the last CTA to finish also folds the per-CTA partials in a
+// fixed order (thread t sums partials t, t+256, ..., then a fixed shared-memory
+// tree) and writes the loss: one launch, deterministic.
 template <class T>
 __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restrict__ pred,
                                                               const T* __restrict__ y, uint64_t n_el,
                                                               double inv_n, T* __restrict__ delta,
-                                                              double* __restrict__ partial) {
+                                                              double* __restrict__ partial,
+                                                              unsigned* __restrict__ counter = nullptr,
+                                                              double scale = 0.0, double* __restrict__ loss = nullptr) {
     __shared__ double red[kThreads];
+    __shared__ int last;
     double s = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n_el;
          i += (uint64_t)gridDim.x * kThreads) {
@@ -203,42 +213,24 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
         __syncthreads();
     }
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
-}
-
-// Fixed-order fold of the per-CTA partials: thread t sums partials t, t+256, ...
-// then a fixed shared-memory tree (deterministic).
-__global__ void __launch_bounds__(256) loss_final_kernel(const double* __restrict__ partial, int count, double scale,
-                                                         double* __restrict__ loss) {
-    __shared__ double red[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < count; i += 256) s += partial[i];
-    red[threadIdx.x] = s;
+    if (!counter) return;
+    __threadfence();
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += kThreads) t += __ldcg(&partial[i]);
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *loss = red[0] * scale;  // mlp.cpp:190: loss *= 0.5 * inv_n
-}
-
-// gb[j] = sum_i delta[i, j]  (f64 accumulation, deterministic row order per column block)
-template <class T>
-__global__ void __launch_bounds__(kThreads) bias_grad_kernel(const T* __restrict__ delta, uint64_t n,
-                                                             uint64_t cols, T* __restrict__ gb) {
-    // CTA = 32 columns x 8 row lanes; each row lane strides over rows, then a
-    // fixed-order smem fold across the 8 lanes.
-    __shared__ double red[8][33];
-    int cx = threadIdx.x % 32, ry = threadIdx.x / 32;
-    uint64_t c = (uint64_t)blockIdx.x * 32 + cx;
-    double s = 0.0;
-    if (c < cols)
-        for (uint64_t r = ry; r < n; r += 8) s += (double)delta[r * cols + c];
-    red[ry][cx] = s;
-    __syncthreads();
-    if (ry == 0 && c < cols) {
-        double t = 0.0;
-        for (int k = 0; k < 8; ++k) t += red[k][cx];
-        gb[c] = (T)t;
+    if (threadIdx.x == 0) {
+        *loss = red[0] * scale;  // mlp.cpp:190: loss *= 0.5 * inv_n
+        *counter = 0;
     }
 }
 
@@ -309,23 +301,21 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     if (blocks > kLossBlocks) blocks = kLossBlocks;
     if (blocks < 1) blocks = 1;
     double inv_n = 1.0 / (double)n;
-    loss_delta_kernel<T><<<blocks, kThreads, 0, d->stream>>>(acts[layers], y, n_el, inv_n, dA, partial);
+    loss_delta_kernel<T><<<blocks, kThreads, 0, d->stream>>>(acts[layers], y, n_el, inv_n, dA, partial,
+                                                             reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n,
+                                                             loss);
     SYNK_LAUNCHED("loss_delta_kernel");
-    loss_final_kernel<<<1, 256, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
-    SYNK_LAUNCHED("loss_final_kernel");
 
     T* delta = dA;
     T* spare = dB;
     for (uint32_t l = layers; l-- > 0;) {
         int64_t din = dims[l], dout = dims[l + 1];
-        // gW = a_l^T delta : M=din, N=dout, K=n
-        if (int rc = gemm<T>(d, EPI_STORE, din, dout, n, acts[l], 1, din, delta, dout, 1,
-                             grad + P.woff[l], dout, nullptr, nullptr, skp);
+        // [gW; gb] = [a_l^T; 1] delta : M=din+1 (row din of A reads as ones), N=dout, K=n;
+        // row din is the bias gradient and lands on b_l (= grad + woff + din*dout)
+        if (int rc = gemm<T>(d, EPI_STORE, din + 1, dout, n, acts[l], 1, din, delta, dout, 1,
+                             grad + P.woff[l], dout, nullptr, nullptr, skp, din);
             rc != SYNK_OK)
             return rc;
-        bias_grad_kernel<T><<<(unsigned)((dout + 31) / 32), kThreads, 0, d->stream>>>(
-            delta, n, dout, grad + P.boff[l]);
-        SYNK_LAUNCHED("bias_grad_kernel");
         if (l > 0) {
             // delta_prev = (delta W^T) * (1 - a_l^2) : M=n, N=din, K=dout
             if (int rc = gemm<T>(d, EPI_TANH_GRAD, n, din, dout, delta, dout, 1, theta + P.woff[l], 1,
@@ -462,10 +452,10 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     double* partial = reinterpret_cast<double*>(base + B.off_partial);
     int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
     const double inv_n = 1.0 / (double)n;
-    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial);
+    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial,
+                                                                 reinterpret_cast<unsigned*>(d->flags_dev + 3),
+                                                                 0.5 * inv_n, loss);
     SYNK_LAUNCHED("loss_delta_kernel");
-    loss_final_kernel<<<1, 256, 0, d->stream>>>(partial, blocks, 0.5 * inv_n, loss);
-    SYNK_LAUNCHED("loss_final_kernel");
     int cur = 0;
     if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd),
                                       wide(L - 1) ? nullptr : bf(B.off_dT), pad8(n));
