@@ -25,6 +25,7 @@ struct synk_dev {
     int* err_dev = nullptr;
     std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
     cudaEvent_t ready = nullptr;     // synk_signal point (no timing), waited on by peers' streams
+    void* graphs = nullptr;          // CUDA-graph cache of the MLP loss/grad launch sequence (mlp.cu)
     int marks_used = 0;
 };
 
@@ -37,6 +38,9 @@ int cuda_fail(cudaError_t err, const char* what);
 // attribute is per-device state (each GPU's context has its own copy of the
 // function), so it is set once per (kernel, device) pair, thread-safely.
 int ensure_max_smem(const void* kernel, int device, int bytes);
+
+// Releases the rank's graph cache (mlp.cu); called by synk_close.
+void release_graphs(synk_dev* d);
 
 #define SYNK_CU(call)                                                   \
     do {                                                                \

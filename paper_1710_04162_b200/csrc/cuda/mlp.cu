@@ -15,6 +15,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <stdlib.h>
+#include <vector>
 
 #include "common.cuh"
 
@@ -488,6 +490,104 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     return SYNK_OK;
 }
 
+// ---- CUDA-graph replay of the loss/grad launch sequence ------------------------------
+// A latency-bound step (config C1: ~12 launches of a few us each) spends as
+// much time in launch overhead as in kernels. The sequence for one set of
+// (shapes, pointers) is captured once into a CUDA graph and replayed with a
+// single launch; in a training loop the stream-ordered pool hands the same
+// batch/gradient buffers back every step, so replays hit. A rank whose
+// pointers keep changing (misses in a row) stops capturing.
+// SYNK_MLP_GRAPHS=0 disables (A/B diagnostics).
+
+struct GraphKey {
+    int dtype;
+    uint32_t layers;
+    uint64_t dims[65];
+    uint64_t n;
+    const void* ptrs[6];
+    bool operator==(const GraphKey& o) const {
+        if (dtype != o.dtype || layers != o.layers || n != o.n) return false;
+        for (uint32_t l = 0; l <= layers && l < 65; ++l)
+            if (dims[l] != o.dims[l]) return false;
+        for (int i = 0; i < 6; ++i)
+            if (ptrs[i] != o.ptrs[i]) return false;
+        return true;
+    }
+};
+
+struct GraphCache {
+    struct Entry {
+        GraphKey key;
+        cudaGraphExec_t exec;
+        uint64_t used;
+    };
+    std::vector<Entry> entries;
+    uint64_t clock = 0;
+    int misses_in_a_row = 0;
+    bool disabled = false;
+    static constexpr size_t kMax = 8;
+    static constexpr int kGiveUp = 16;
+};
+
+template <class F>
+int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
+    static const bool enabled = [] {
+        const char* e = getenv("SYNK_MLP_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled) return launch_all();
+    if (!d->graphs) d->graphs = new GraphCache();
+    GraphCache& gc = *static_cast<GraphCache*>(d->graphs);
+    if (gc.disabled) return launch_all();
+    for (auto& e : gc.entries)
+        if (e.key == key) {
+            e.used = ++gc.clock;
+            gc.misses_in_a_row = 0;
+            SYNK_CU(cudaGraphLaunch(e.exec, d->stream));
+            return SYNK_OK;
+        }
+    if (++gc.misses_in_a_row > GraphCache::kGiveUp) {
+        gc.disabled = true;
+        return launch_all();
+    }
+    cudaGraph_t graph = nullptr;
+    SYNK_CU(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = launch_all();
+    const cudaError_t ec = cudaStreamEndCapture(d->stream, &graph);
+    if (rc != SYNK_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (ec != cudaSuccess) return synk::cuda_fail(ec, "cudaStreamEndCapture (mlp loss/grad)");
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return synk::cuda_fail(ei, "cudaGraphInstantiate (mlp loss/grad)");
+    if (gc.entries.size() == GraphCache::kMax) {
+        auto lru = std::min_element(gc.entries.begin(), gc.entries.end(),
+                                    [](const GraphCache::Entry& a, const GraphCache::Entry& b) { return a.used < b.used; });
+        cudaGraphExecDestroy(lru->exec);
+        gc.entries.erase(lru);
+    }
+    gc.entries.push_back({key, exec, ++gc.clock});
+    SYNK_CU(cudaGraphLaunch(exec, d->stream));
+    return SYNK_OK;
+}
+
+}  // namespace
+
+namespace synk {
+void release_graphs(synk_dev* d) {
+    if (!d->graphs) return;
+    auto* gc = static_cast<GraphCache*>(d->graphs);
+    for (auto& e : gc->entries) cudaGraphExecDestroy(e.exec);
+    delete gc;
+    d->graphs = nullptr;
+}
+}  // namespace synk
+
+namespace {
+
 }  // namespace
 
 extern "C" {
@@ -538,11 +638,21 @@ int synk_mlp_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t la
     if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
     SYNK_REQUIRE(workspace_bytes >= ws_bytes(dtype, p, n), SYNK_EARG, "mlp: workspace too small");
     synk::DeviceGuard g(d->device);
-    if (dtype == SYNK_F32)
-        return loss_grad_t<float>(d, dims, layers, p, (const float*)params, (const float*)x,
-                                  (const float*)y, n, loss_dev, (float*)grad, workspace);
-    return loss_grad_t<double>(d, dims, layers, p, (const double*)params, (const double*)x,
-                               (const double*)y, n, loss_dev, (double*)grad, workspace);
+    auto launch_all = [&]() {
+        if (dtype == SYNK_F32)
+            return loss_grad_t<float>(d, dims, layers, p, (const float*)params, (const float*)x,
+                                      (const float*)y, n, loss_dev, (float*)grad, workspace);
+        return loss_grad_t<double>(d, dims, layers, p, (const double*)params, (const double*)x,
+                                   (const double*)y, n, loss_dev, (double*)grad, workspace);
+    };
+    GraphKey key{};
+    key.dtype = dtype;
+    key.layers = layers;
+    for (uint32_t l = 0; l <= layers && l < 65; ++l) key.dims[l] = dims[l];
+    key.n = n;
+    key.ptrs[0] = params, key.ptrs[1] = x, key.ptrs[2] = y, key.ptrs[3] = loss_dev, key.ptrs[4] = grad;
+    key.ptrs[5] = workspace;
+    return graph_launch(d, key, launch_all);
 }
 
 }  // extern "C"

@@ -150,6 +150,7 @@ int synk_close(synk_dev* d) {
     cudaFreeHost(const_cast<int*>(d->err_host));
     for (cudaEvent_t e : d->marks) cudaEventDestroy(e);
     if (d->ready) cudaEventDestroy(d->ready);
+    release_graphs(d);
     delete d;
     return SYNK_OK;
 }
