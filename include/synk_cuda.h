@@ -184,6 +184,13 @@ int synk_tree_reduce(synk_dev* dev, int world, int dtype, int op, const void* co
 /* Rank r copies chunk r of bufs[src] into every other replica
  * (ReplicatedVariable::broadcast, replicated.cpp:115-122). */
 int synk_broadcast(synk_dev* dev, int world, int src, void* const* bufs, uint64_t bytes);
+/* Small-buffer forms: ONE rank runs every chunk of the collective over the
+ * peer pointers (same per-element tree order, so bitwise identical to the
+ * per-rank forms). For buffers where waking every rank's thread costs more
+ * than the transfer (ReplicatedVariable::all_reduce / broadcast below 1 MiB,
+ * replicated.cpp:115-137). */
+int synk_all_reduce_whole(synk_dev* dev, int world, int dtype, int op, void* const* bufs, uint64_t n);
+int synk_broadcast_whole(synk_dev* dev, int world, int src, void* const* bufs, uint64_t bytes);
 
 /* ---- optimizer ---------------------------------------------------------------- */
 /* hyper: momentum {mu}; rmsprop {rho, eps}; adam {beta1, beta2, eps}.

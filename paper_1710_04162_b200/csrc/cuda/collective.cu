@@ -302,11 +302,11 @@ int fill_ptrs(Ptrs* out, void* const* bufs, int w) {
 }
 
 template <class T>
-int allreduce_t(synk_dev* d, int w, int op, void* const* bufs, uint64_t n) {
+int allreduce_t(synk_dev* d, int w, int op, void* const* bufs, uint64_t n, bool whole = false) {
     Ptrs P{};
     if (int rc = fill_ptrs(&P, bufs, w); rc != SYNK_OK) return rc;
-    uint64_t lo, hi;
-    chunk_of(n, w, d->rank, &lo, &hi);
+    uint64_t lo = 0, hi = n;
+    if (!whole) chunk_of(n, w, d->rank, &lo, &hi);
     if (lo >= hi) return SYNK_OK;
     double inv_w = 1.0 / (double)w;
     bool vec = ptrs_aligned16(bufs, w);
@@ -408,6 +408,16 @@ int synk_all_reduce(synk_dev* d, int world, int dtype, int op, void* const* bufs
                              : allreduce_t<double>(d, world, op, bufs, n);
 }
 
+int synk_all_reduce_whole(synk_dev* d, int world, int dtype, int op, void* const* bufs, uint64_t n) {
+    SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_all_reduce: bad dtype");
+    SYNK_REQUIRE(op >= SYNK_OP_SUM && op <= SYNK_OP_PROD, SYNK_EARG,
+                 "all_reduce: Gather is not a reduction (use gather())");
+    if (n == 0) return SYNK_OK;
+    synk::DeviceGuard g(d->device);
+    return dtype == SYNK_F32 ? allreduce_t<float>(d, world, op, bufs, n, true)
+                             : allreduce_t<double>(d, world, op, bufs, n, true);
+}
+
 int synk_tree_reduce(synk_dev* d, int world, int dtype, int op, const void* const* bufs, uint64_t n,
                      void* out) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_tree_reduce: bad dtype");
@@ -427,20 +437,28 @@ int synk_tree_reduce(synk_dev* d, int world, int dtype, int op, const void* cons
     return SYNK_OK;
 }
 
-int synk_broadcast(synk_dev* d, int world, int src, void* const* bufs, uint64_t bytes) {
+static int broadcast_impl(synk_dev* d, int world, int src, void* const* bufs, uint64_t bytes, bool whole) {
     SYNK_REQUIRE(src >= 0 && src < world, SYNK_EARG, "broadcast: src rank out of range");
     if (bytes == 0 || world == 1) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     Ptrs P{};
     if (int rc = fill_ptrs(&P, bufs, world); rc != SYNK_OK) return rc;
-    uint64_t lo, hi;
-    chunk_of(bytes, world, d->rank, &lo, &hi);  // byte chunks, 16-byte multiples
+    uint64_t lo = 0, hi = bytes;
+    if (!whole) chunk_of(bytes, world, d->rank, &lo, &hi);  // byte chunks, 16-byte multiples
     if (lo >= hi) return SYNK_OK;
     bool vec = ptrs_aligned16(bufs, world) && hi % 16 == 0;
     unsigned grid = synk::grid_for(d, vec ? (hi - lo) / 16 + 1 : hi - lo, kBlock);
     bcast_chunk_kernel<<<grid, kBlock, 0, d->stream>>>(P, world, src, lo, hi, vec);
     SYNK_LAUNCHED("bcast_chunk_kernel");
     return SYNK_OK;
+}
+
+int synk_broadcast(synk_dev* d, int world, int src, void* const* bufs, uint64_t bytes) {
+    return broadcast_impl(d, world, src, bufs, bytes, false);
+}
+
+int synk_broadcast_whole(synk_dev* d, int world, int src, void* const* bufs, uint64_t bytes) {
+    return broadcast_impl(d, world, src, bufs, bytes, true);
 }
 
 int synk_optimizer_step(synk_dev* d, int dtype, int rule, const double* hyper, double lr, uint64_t t,

@@ -11,6 +11,12 @@
 
 namespace synkpar {
 
+namespace {
+// Collectives up to this size run as one kernel on rank 0's GPU (latency
+// bound: a launch + a sync instead of a phase over every rank thread).
+constexpr std::size_t kWholeCollectiveBytes = std::size_t(1) << 20;
+} // namespace
+
 namespace detail {
 
 
@@ -114,6 +120,16 @@ void ReplicatedVariable::broadcast(std::size_t src) {
     }
     std::vector<void*> ptrs = replica_ptrs(rec);
     const std::size_t bytes = s.byte_size();
+    if (bytes <= kWholeCollectiveBytes) {
+        // Small buffer: rank 0's GPU copies every chunk over the peer pointers
+        // (all streams are idle between phases), no rank thread is woken.
+        detail::check(synk_broadcast_whole(st.handles[0], static_cast<int>(st.world), static_cast<int>(src),
+                                           ptrs.data(), bytes),
+                      "broadcast");
+        detail::dev_sync(st.ranks[0]);
+        rec.coherent = true;
+        return;
+    }
     detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
         detail::check(synk_broadcast(st.handles[r], static_cast<int>(st.world), static_cast<int>(src), ptrs.data(), bytes),
                       "broadcast");
@@ -130,6 +146,19 @@ void ReplicatedVariable::all_reduce(ReduceOp op) {
     std::vector<void*> ptrs = replica_ptrs(rec);
     const std::size_t n = rec.replicas[0].size();
     const int dt = detail::synk_dtype(rec.replicas[0].dtype());
+    if (rec.replicas[0].byte_size() <= kWholeCollectiveBytes) {
+        // Small buffer: one kernel on rank 0's GPU folds every chunk (same
+        // per-element tree order) and writes all replicas over the peer
+        // pointers -- no rank thread is woken, one launch + one sync.
+        detail::require_idle(st, "all_reduce");
+        require_same_dtype(rec);
+        detail::check(synk_all_reduce_whole(st.handles[0], static_cast<int>(st.world), dt, detail::synk_op(op),
+                                            ptrs.data(), n),
+                      "all_reduce");
+        detail::dev_sync(st.ranks[0]);
+        rec.coherent = true;
+        return;
+    }
     detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
         require_same_dtype(rec);
         detail::check(synk_all_reduce(st.handles[r], static_cast<int>(st.world), dt, detail::synk_op(op), ptrs.data(), n),
