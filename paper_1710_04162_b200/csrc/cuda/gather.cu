@@ -286,11 +286,12 @@ extern "C" int synk_gather_rows(synk_dev* d, const void* src, uint64_t src_rows,
     if (n_idx == 0 || row_bytes == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     uint64_t a = row_bytes | (uint64_t)(uintptr_t)src | (uint64_t)(uintptr_t)dst;
-    // Diagnostics: SYNK_GATHER_VEC / SYNK_GATHER_BULK force one kernel (A/B runs).
-    static const bool force_vec = getenv("SYNK_GATHER_VEC") != nullptr;
+    // The cp.async.bulk kernel is opt-in (SYNK_GATHER_BULK=1): measured slower
+    // than the vector kernel at 1 KiB rows (0.87 vs 0.91 of HBM: per-request
+    // TMA cost) and on the C5 batch (8 KiB rows, 8192 rows: 32.8 vs 23.2 us);
+    // it only won on very large 4 KiB-row launches (5,600 vs 5,494 GB/s).
     static const bool force_bulk = getenv("SYNK_GATHER_BULK") != nullptr;
-    const bool bulk_ok = (a & 15) == 0 && row_bytes <= 8192;
-    if (bulk_ok && !force_vec && (force_bulk || row_bytes >= 4096))
+    if (force_bulk && (a & 15) == 0 && row_bytes <= 8192)
         return launch_bulk(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 15) == 0) return launch<16>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 7) == 0) return launch<8>(d, src, src_rows, row_bytes, idx, n_idx, dst);

@@ -93,9 +93,10 @@ def _pinned_copy(arr):
 
 
 @pytest.mark.parametrize("idx_in", ["hbm", "pinned"])
-def test_gather_wide_rows_bulk_path(oracle, idx_in):
-    """Rows of 4-8 KiB take the cp.async.bulk (TMA engine) kernel; index lists
-    may sit in HBM or in pinned host memory (read in place over PCIe)."""
+def test_gather_wide_rows(oracle, idx_in):
+    """Rows of 4-8 KiB (odd sizes too); index lists in HBM or in pinned host
+    memory (read in place over PCIe). Run again with SYNK_GATHER_BULK=1 by
+    test_gather_bulk_kernel_subprocess for the cp.async.bulk kernel."""
     rng = np.random.default_rng(3)
     with Ranks(1) as R:
         for dtype, shape in ((np.float32, (3000, 1024)), (np.float64, (500, 1024)), (np.float32, (257, 2048)),
@@ -120,6 +121,21 @@ def test_gather_wide_rows_bulk_path(oracle, idx_in):
                                          _u64(bad.size), _vp(d_out)), "gather")
             assert R.sync() == -1  # SYNK_EBOUNDS
             assert R.sync() == 0
+
+
+def test_gather_bulk_kernel_subprocess():
+    """The opt-in cp.async.bulk (TMA engine) gather (SYNK_GATHER_BULK=1 is read
+    once per process): the wide-row and small-row parity tests in a child."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SYNK_GATHER_BULK="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", os.path.join(here, "test_gpu_kernels.py"),
+                          "-k", "gather and not subprocess"], env=env, capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(here))
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
 def test_gather_index_list_in_pinned_host_memory(oracle):
