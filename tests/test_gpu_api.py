@@ -547,3 +547,69 @@ def test_c3_full_scale_slicing_aggregation(sk, oracle, world):
     err = float(np.max(np.abs(s.astype(np.float64) - exact)))
     assert err <= 16 * 2.0 ** -23 * np.sqrt(rows), err
     assert oracle.elem_err(s, exact) <= rows * 2.0 ** -23
+
+
+def _c2_pattern(rows, cols):
+    """Exact-integer f32 rows (< 2^24): column 0 is the row index, so a gathered
+    row identifies its source row; computable for any row subset."""
+    r = np.asarray(rows, np.int32)[:, None]
+    c = np.arange(cols, dtype=np.int32)[None, :] * np.int32(1009)
+    return ((r + c) & np.int32(0xFFFFFF)).astype(np.float32)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_c2_full_scale_indexed_gather(sk, world):
+    """C2 at BASELINE size: 10,000,000 x 256 f32 shared dataset (10.24 GB,
+    pinned host store + HBM mirror), 64 x 4096-row shuffled batches per rank,
+    index list pinned (read in place by the gather kernel): every gathered
+    row bit-exact; a bad index at full size raises BoundsError, pool alive."""
+    rows, cols = 10_000_000, 256
+    arr = sk.SharedInput.alloc([rows, cols], "f32")
+    block = 1 << 18
+    for r0 in range(0, rows, block):
+        r1 = min(rows, r0 + block)
+        arr.write(r0, r1, _c2_pattern(np.arange(r0, r1), cols))
+    rng = np.random.default_rng(11)
+    n = 4096 * 64 * world
+    idx = sk.pinned_array(n, "int64")
+    idx[:] = rng.integers(0, rows, n)
+    idx[:2] = [0, rows - 1]
+    with sk.Pool(workers=world) as pool:
+        arr.mirror(pool)
+        f = sk.make_function(pool, sk.identity_kernel(), ["scatter"], ["gather"])
+        cnt = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
+        sk.distribute(pool)
+        (got,) = f.call([arr], indexes=idx)
+        assert got.tobytes() == _c2_pattern(np.asarray(idx), cols).tobytes()
+        assert float(cnt.call([arr], indexes=idx)[0]) == n
+        idx[n // 2] = rows
+        with pytest.raises(sk.BoundsError):
+            cnt.call([arr], indexes=idx)
+        assert pool.alive
+
+
+def test_c4_full_scale_all_reduce_broadcast(sk):
+    """C4 at its largest size: 1 GiB f32 replicas, W=2 (both ranks on one GPU
+    here; the same peer-memory kernels cross NVLink on a multi-GPU box).
+    all_reduce mean == (a + b) * 0.5 bit for bit (the reference's W=2 tree),
+    max bit for bit, broadcast bit for bit, replicas coherent."""
+    n = (1 << 30) // 4
+    rng = np.random.default_rng(4)
+    a = rng.random(n, dtype=np.float32) * 2 - 1
+    b = rng.random(n, dtype=np.float32) * 2 - 1
+    with sk.Pool(workers=2, devices=[0, 0]) as pool:
+        var = sk.replicate(pool, np.zeros(1, np.float32))
+        var.set(0, a)
+        var.set(1, b)
+        var.all_reduce("mean")
+        assert var.coherent
+        want = (a + b) * np.float32(0.5)
+        assert var.get(1).tobytes() == want.tobytes()
+        var.set(0, a)
+        var.set(1, b)
+        var.all_reduce("max")
+        assert var.get(0).tobytes() == np.maximum(a, b).tobytes()
+        var.set(0, b)
+        var.broadcast(0)
+        assert var.get(1).tobytes() == b.tobytes()
+        assert var.coherent
