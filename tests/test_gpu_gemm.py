@@ -253,3 +253,48 @@ def test_bf16_mn_major_fused_epilogues():
             act = bf16_round(np.tanh(rng.uniform(-1, 1, (M, N))))
             got = gemm_layout(R, a, b, layout, "tanh_grad", act=act, out_bf16=True)
             assert rel_err(got, z * (1 - act.astype(np.float64) ** 2)) <= 2.0 ** -7 * 4
+
+
+def test_c5_full_size_bf16_gradient_vs_fp64(sk, oracle):
+    """C5 at BASELINE size: MLP 2048-4096-4096-100 (25,583,716 params), batch
+    8192, every product on tcgen05 in bf16. Reference: the same loss/gradient
+    math (mlp.cpp:134-218) in fp64 with torch on the GPU (a floating-point
+    cross-check of a floating-point kernel). Bars as the small-config test:
+    relative Frobenius error of the gradient <= 2e-2, loss <= 1e-2; then one
+    SGD step through the Trainer is bit-for-bit the reference's update rule
+    (sgd.cpp:46-52 restated in the oracle) applied to the gradient block."""
+    import torch
+
+    dims = [2048, 4096, 4096, 100]
+    cfg = sk.MlpConfig(in_dim=dims[0], width=dims[1], out_dim=dims[3], layers=3, seed=1)
+    x, y = sk.mlp_make_dataset(8192, cfg, seed=2, dtype="f32")
+    params = sk.mlp_init_params(cfg, "f32")
+    dev = torch.device("cuda:0")
+    P = [torch.from_numpy(p.astype(np.float64)).to(dev) for p in params]
+    a = [torch.from_numpy(x.astype(np.float64)).to(dev)]
+    for l in range(3):
+        z = a[-1] @ P[2 * l] + P[2 * l + 1]
+        a.append(torch.tanh(z) if l < 2 else z)
+    yt = torch.from_numpy(y.astype(np.float64)).to(dev)
+    n = x.shape[0]
+    ref_loss = float(0.5 / n * ((a[3] - yt) ** 2).sum())
+    delta = (a[3] - yt) / n
+    grads = [None] * 6
+    for l in (2, 1, 0):
+        grads[2 * l] = a[l].T @ delta
+        grads[2 * l + 1] = delta.sum(0)
+        if l > 0:
+            delta = (delta @ P[2 * l].T) * (1 - a[l] ** 2)
+    ref_grad = torch.cat([g.reshape(-1) for g in grads]).cpu().numpy()
+    with sk.Pool(workers=1) as pool:
+        block = sk.ParamBlock.create(pool, params)
+        f = sk.mlp_grad_function(pool, block, compute="bf16")
+        sk.distribute(pool)
+        (loss,) = f.call([x, y])
+        g = block.grads.get(0).astype(np.float64)
+        assert abs(loss - ref_loss) / ref_loss <= 1e-2
+        assert np.linalg.norm(g - ref_grad) / np.linalg.norm(ref_grad) <= 2e-2
+        p0 = block.params.get(0)
+        trainer = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
+        trainer.train_step(f, [x, y])
+        assert block.params.get(0).tobytes() == oracle.sgd(p0, block.grads.get(0), 0.01).tobytes()
