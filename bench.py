@@ -106,6 +106,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if self.gpus <= 0:  # a non-zero torchrun rank: rank 0 samples every GPU of the box
+            return self
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -197,7 +199,7 @@ def workload_config(args, n_gpus):
     return {"workload": "indexed gather: shuffled %d-row batches from a %dx%d fp32 shared dataset" % (
         args.batch, args.rows, args.cols), "batches_per_step_per_gpu": args.batches,
         "rows_per_step": args.batch * args.batches * n_gpus, "row_bytes": args.cols * 4,
-        "parallelism": "dp%d (one rank per GPU, single-process executor)" % n_gpus,
+        "parallelism": "dp%d (one rank per GPU; under torchrun one process per GPU for this headline)" % n_gpus,
         "l2": "inputs larger than L2 (10.24 GB dataset, 2 rotating 256 MiB outputs per GPU)"}
 
 
@@ -280,7 +282,8 @@ def collectives_c4(sk, args, n_gpus):
     With one GPU the W=2 ranks share it, so the peer-memory kernels move the
     bytes through local HBM instead of NVLink (stated in the output)."""
     world = n_gpus if n_gpus >= 2 else 2
-    devices = list(range(n_gpus)) if n_gpus >= 2 else [0, 0]
+    ndev = max(1, sk.device_count())
+    devices = [d % ndev for d in range(n_gpus)] if n_gpus >= 2 else [0, 0]
     sizes = [1 << k for k in range(10, 31, 3)] + [1 << 30]
     rng = np.random.default_rng(1000)
     sweep = []
@@ -308,8 +311,8 @@ def collectives_c4(sk, args, n_gpus):
                           "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9, "coherent": coherent})
     out = {"config": "C4: all_reduce mean + broadcast(0) of f32 buffers 1 KiB - 1 GiB, W=%d ranks" % world,
            "ranks": world, "devices": devices,
-           "link": "NVLink peer memory" if n_gpus >= 2 else "1 GPU: both ranks share it, peer-memory kernels run "
-                                                             "over local HBM (NVLink unmeasured)",
+           "link": "NVLink peer memory" if len(set(devices)) >= 2 else "1 GPU: the ranks share it, peer-memory "
+                                                                         "kernels run over local HBM (NVLink unmeasured)",
            "sweep": sweep}
     if not args.no_cpu_baseline:
         ref = []
@@ -325,7 +328,11 @@ def collectives_c4(sk, args, n_gpus):
     return out
 
 
-def ours(args, n_gpus):
+def gather_headline(args, n_gpus, devices, dist, world):
+    """C2 headline on this process's GPUs (`devices`): value / e2e / roofline.
+    Under torchrun every rank runs this on its own GPU with its own one-GPU
+    pool (the path partitions: no data-path collective); times are the max
+    over ranks, bytes the sum."""
     import paper_1710_04162_b200 as sk
 
     lib = ctypes.CDLL(os.path.join(ROOT, "paper_1710_04162_b200", "_lib", "libsynk_cuda.so"))
@@ -343,15 +350,16 @@ def ours(args, n_gpus):
 
     t_setup = time.time()
     arr = fill_dataset(sk, rows, cols)
-    pool = sk.Pool(workers=n_gpus, devices=list(range(n_gpus)))
+    pool = sk.Pool(workers=len(devices), devices=list(devices))
+    n_local = len(devices)
     arr.mirror(pool)
     setup_s = time.time() - t_setup
 
-    handles = [vp(pool.device_handle(r)) for r in range(n_gpus)]
+    handles = [vp(pool.device_handle(r)) for r in range(n_local)]
     rng = np.random.default_rng(11)
     total_steps = args.warmup + args.steps
     idx_dev, dst_dev, mirrors = [], [], []
-    for r in range(n_gpus):
+    for r in range(n_local):
         h = handles[r]
         idx = rng.integers(0, rows, total_steps * n_step).astype(np.uint64)
         p = vp()
@@ -370,11 +378,11 @@ def ours(args, n_gpus):
     def gather_launches(step_rows, steps, warm, per_launch_marks=True):
         """Launch `steps` gathers of step_rows rows per GPU; return (max over GPUs of
         the device time of the timed region, mean per-launch kernel time)."""
-        marks = [[] for _ in range(n_gpus)]
-        for r in range(n_gpus):
+        marks = [[] for _ in range(n_local)]
+        for r in range(n_local):
             ok(lib.synk_mark_reset(handles[r]), "marks")
         for s in range(warm + steps):
-            for r in range(n_gpus):
+            for r in range(n_local):
                 h = handles[r]
                 m = ctypes.c_int()
                 if s >= warm:
@@ -387,7 +395,7 @@ def ours(args, n_gpus):
                     ok(lib.synk_mark(h, ctypes.byref(m)), "mark")
                     marks[r].append(m.value)
         region, launch = [], []
-        for r in range(n_gpus):
+        for r in range(n_local):
             ok(lib.synk_sync(handles[r]), "sync")
             sec = ctypes.c_double()
             ok(lib.synk_mark_elapsed(handles[r], marks[r][0], marks[r][-1], ctypes.byref(sec)), "elapsed")
@@ -399,15 +407,31 @@ def ours(args, n_gpus):
             launch.append(tot / steps)
         return max(region), float(np.mean(launch))
 
-    with ClockSampler(n_gpus) as clocks:
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    sampler = ClockSampler(n_gpus) if not dist or dist.get_rank() == 0 else ClockSampler(0)
+    with sampler as clocks:
         # Soak under the same load first so nvidia-smi (200 ms cadence) samples
         # clocks around the timed region even when K steps take milliseconds.
         t_soak = time.time()
         while time.time() - t_soak < 1.5:
             gather_launches(n_step, 16, 0)
+        barrier()
         region_s, launch_s = gather_launches(n_step, args.steps, args.warmup)
+        region_s, launch_s = max_over_ranks(region_s), max_over_ranks(launch_s)
         time.sleep(0.25)
-    bytes_step = n_gpus * n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA)
+    bytes_step = world * n_local * n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA)  # all GPUs of the job
     value = bytes_step * args.steps / region_s / 1e9
     achieved = n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA) / launch_s / 1e9
     # latency of a single 4096-row batch (the per-call granularity of the config)
@@ -421,17 +445,18 @@ def ours(args, n_gpus):
     # data loader would hand them over).
     e2e_idx = []
     for _ in range(total_steps):
-        buf = sk.pinned_array(n_step * n_gpus, "int64")
-        buf[:] = rng.integers(0, rows, n_step * n_gpus)
+        buf = sk.pinned_array(n_step * n_local, "int64")
+        buf[:] = rng.integers(0, rows, n_step * n_local)
         e2e_idx.append(buf)
     for s in range(args.warmup):
         (cnt,) = f.call([arr], indexes=e2e_idx[s])
-        assert float(cnt) == n_step * n_gpus
+        assert float(cnt) == n_step * n_local
+    barrier()
     t0 = time.perf_counter()
     for s in range(args.warmup, total_steps):
         (cnt,) = f.call([arr], indexes=e2e_idx[s])
-    e2e_s = time.perf_counter() - t0
-    assert float(cnt) == n_step * n_gpus
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    assert float(cnt) == n_step * n_local
     e2e = bytes_step * args.steps / e2e_s / 1e9
     # where the e2e time goes (untimed repeat with the call report)
     rep_acc = {"scatter_s": 0.0, "reduce_s": 0.0, "total_s": 0.0, "compute_s": 0.0}
@@ -442,6 +467,23 @@ def ours(args, n_gpus):
         rep_acc["compute_s"] += max(rep["rank_compute_s"]) / args.steps
     e2e_breakdown = {k + "_us": 1e6 * v for k, v in rep_acc.items()}
 
+    pool.shutdown()
+    del arr
+    return {"value": value, "region_s": region_s, "e2e": e2e, "e2e_breakdown": e2e_breakdown, "achieved": achieved,
+            "single_s": single_s, "clocks": clocks.summary(),
+            "setup_s": setup_s, "n_step": n_step, "row_bytes": row_bytes, "peak": peak, "peak_kind": peak_kind}
+
+
+def sub_measurements(args, n_gpus, peak, peak_kind):
+    """C1, C5 (sync SGD through Trainer), C3 (slicing), C4 (collectives): the
+    executor's own single-process pool over the job's GPUs (the paper's
+    master + workers; collectives are peer-memory kernels across them)."""
+    import paper_1710_04162_b200 as sk
+
+    ndev = max(1, sk.device_count())
+    pool = sk.Pool(workers=n_gpus, devices=[d % ndev for d in range(n_gpus)])
+    rng = np.random.default_rng(12)
+    total_steps = args.warmup + args.steps
     # ---- sync SGD (C1) sub-measurement ------------------------------------------------
     sgd = None
     if not args.no_sgd:
@@ -521,27 +563,47 @@ def ours(args, n_gpus):
     c4 = None
     if not args.no_c4:
         c4 = collectives_c4(sk, args, n_gpus)
+    out = {}
+    if sgd:
+        out["sync_sgd"] = sgd
+    if sgd5:
+        out["sync_sgd_wide_bf16"] = sgd5
+    if c3:
+        out["slicing_c3"] = c3
+    if c4:
+        out["collectives_c4"] = c4
+    return out
+
+
+def ours(args, n_gpus, dist=None, world=1, local_device=0):
+    """Our arm. Single process: the headline on a pool over all N GPUs. Under
+    torchrun: one process per GPU for the headline (each its own one-GPU
+    pool), then rank 0 alone runs the sub-measurements over every GPU."""
+    devices = [local_device] if dist is not None else list(range(n_gpus))
+    hd = gather_headline(args, n_gpus, devices, dist, world)
+    if dist is not None:
+        dist.barrier()  # every rank's headline pool is down before rank 0 opens its own over all GPUs
+        if dist.get_rank() != 0:
+            return None
+    value, n_step, row_bytes = hd["value"], hd["n_step"], hd["row_bytes"]
+    achieved, peak, peak_kind = hd["achieved"], hd["peak"], hd["peak_kind"]
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": n_gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * region_s / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * hd["region_s"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, n_gpus),
-            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 8 * n_step * n_gpus,
-                    "d2h_bytes_per_step": 8, "path": "Function.call(indexes) -> row_count kernel -> Sum",
-                    "breakdown_per_call": e2e_breakdown},
+            "e2e": {"value": hd["e2e"], "unit": "GB/s", "h2d_bytes_per_step": 8 * n_step * n_gpus,
+                    "d2h_bytes_per_step": 8 * (world if dist is not None else 1),
+                    "path": "Function.call(indexes) -> row_count kernel -> Sum",
+                    "breakdown_per_call": hd["e2e_breakdown"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n_step * (2 * row_bytes + 8)),
                          "traffic_unit": "bytes/launch", "peak_kind": peak_kind,
                          "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
-            "single_batch_us": 1e6 * single_s,
-            "gpu_launches": n_gpus * args.steps, "clocks": clocks.summary(), "setup_s": setup_s}
-    if sgd:
-        line["sync_sgd"] = sgd
-    if sgd5:
-        line["sync_sgd_wide_bf16"] = sgd5
-    if c3:
-        line["slicing_c3"] = c3
-    if c4:
-        line["collectives_c4"] = c4
+            "single_batch_us": 1e6 * hd["single_s"],
+            "gpu_launches": n_gpus * args.steps, "clocks": hd["clocks"], "setup_s": hd["setup_s"]}
+    if dist is not None:
+        line["processes"] = "one per GPU for the headline (torchrun); rank 0 alone for the sub-measurements"
+    line.update(sub_measurements(args, n_gpus, peak, peak_kind))
     return line
 
 
@@ -561,6 +623,12 @@ def main():
             seen = [{"rank": 0, "pid": os.getpid()}]
         line = {"metric": METRIC, "dry_run": True, "n_gpus": n_gpus, "world": world,
                 "ranks_seen": sorted(s["rank"] for s in seen), "driver_rank": 0}
+    elif args.impl == "ours" and dist is not None:
+        # torchrun: one process per GPU for the headline, rank 0 then drives the rest
+        import paper_1710_04162_b200 as sk
+
+        local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, sk.device_count())
+        line = ours(args, n_gpus, dist=dist, world=world, local_device=local)
     elif rank == 0:
         if args.impl == "reference":
             line = reference_arm(args, n_gpus)
