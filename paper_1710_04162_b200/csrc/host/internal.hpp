@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdint>
 #include <functional>
+#include <istream>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -62,6 +63,15 @@ DevBuffer dev_clone(const std::shared_ptr<RankDevice>& rd, const DevBuffer& src)
 void dev_sync(const std::shared_ptr<RankDevice>& rd);
 int synk_dtype(DType dt);
 int synk_op(ReduceOp op);
+
+// SYNK container streaming (tensor_io.cpp): the header, then the payload read
+// straight into its destination (pinned SharedInput store or an NdBuffer).
+struct TensorHeader {
+    std::vector<std::size_t> shape;
+    DType dtype = DType::Float64;
+};
+TensorHeader read_tensor_header(std::istream& in);
+void read_tensor_payload(std::istream& in, std::byte* dst, std::size_t bytes);
 
 // Lazily opened context on GPU 0 for host-buffer API helpers (step_*, mlp_loss_grad).
 std::shared_ptr<RankDevice> utility_device();

@@ -115,3 +115,39 @@ def test_synk_bytes_match_reference_writer(sk, oracle):
         with tempfile.TemporaryDirectory() as d:
             ref.save_tensor(os.path.join(d, "r.synk"), arr)
             assert open(os.path.join(d, "r.synk"), "rb").read() == sk.tensor_to_bytes(arr)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_synk_streamed_io_and_shared_input_from_file(sk, tmp_path, dtype):
+    """SYNK I/O streams: save writes header + payload in place, load_tensor and
+    SharedInput.from_file read the payload straight into the destination (the
+    pinned store for from_file, shared_input.cpp:75-82). Same bytes, same
+    IoError cases (truncated header / extents / payload, bad magic/version/dtype)."""
+    path = str(tmp_path / "x.synk")
+    data = np.random.default_rng(1).standard_normal((257, 33)).astype(dtype)
+    sk.save_tensor(path, data)
+    blob = open(path, "rb").read()
+    assert blob == sk.tensor_to_bytes(data)
+    np.testing.assert_array_equal(sk.load_tensor(path), data)
+    arr = sk.SharedInput.from_file(path)
+    assert arr.shape == [257, 33] and arr.capacity == data.size
+    assert arr.array().tobytes() == data.tobytes()
+    big = sk.SharedInput.from_file(path, capacity=data.size * 2)
+    assert big.capacity == data.size * 2 and big.array().tobytes() == data.tobytes()
+    cases = {
+        blob[:5]: "header incomplete",
+        blob[:8 + 8]: "extents incomplete",
+        blob[:-1]: "payload incomplete",
+        b"NOPE" + blob[4:]: "wrong magic",
+        blob[:4] + b"\x02" + blob[5:]: "version",
+        blob[:5] + b"\x07" + blob[6:]: "dtype code",
+    }
+    for bad, msg in cases.items():
+        with open(path, "wb") as fh:
+            fh.write(bad)
+        for load in (sk.load_tensor, sk.SharedInput.from_file):
+            with pytest.raises(sk.IoError, match=msg):
+                load(path)
+    with open(path, "wb") as fh:
+        fh.write(blob + b"trailing")  # the reference ignores bytes past the payload
+    np.testing.assert_array_equal(sk.load_tensor(path), data)
