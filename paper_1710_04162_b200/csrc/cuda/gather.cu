@@ -52,8 +52,6 @@ struct Vec<1> {
     static __device__ __forceinline__ T load(const T* p) { return __ldg(p); }
 };
 
-constexpr int kRows = 4;    // rows in flight per warp
-constexpr int kUnroll = 2;  // vectors per row in flight per lane
 constexpr int kBlock = 256;
 
 // Chunked grid-stride: warp w takes chunks w, w + nwarps, ... of `chunk`
@@ -63,8 +61,9 @@ constexpr int kBlock = 256;
 // sits in pinned host memory and travels over PCIe), and the NEXT chunk's
 // indices are requested before the current chunk's rows are streamed, so the
 // index fetch overlaps a chunk of row traffic.
-template <int BYTES>
-__global__ void __launch_bounds__(kBlock) gather_rows_kernel(
+// kRows rows in flight per warp, kUnroll 16-byte vectors per row per lane.
+template <int BYTES, int kRows = 4, int kUnroll = 2, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
     const typename Vec<BYTES>::T* __restrict__ src, uint64_t src_rows, uint64_t row_vecs,
     const uint64_t* __restrict__ idx, uint64_t n_idx, uint32_t chunk, typename Vec<BYTES>::T* __restrict__ dst,
     int* __restrict__ err) {
@@ -118,19 +117,28 @@ __global__ void __launch_bounds__(kBlock) gather_rows_kernel(
     }
 }
 
+template <int BYTES, int R, int U, int MB>
+void launch_variant(synk_dev* d, unsigned blocks, const void* src, uint64_t src_rows, uint64_t row_bytes,
+                    const uint64_t* idx, uint64_t n_idx, uint32_t chunk, void* dst) {
+    using V = typename Vec<BYTES>::T;
+    gather_rows_kernel<BYTES, R, U, MB><<<blocks, kBlock, 0, d->stream>>>(
+        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, chunk, (V*)dst, d->err_dev);
+}
+
 template <int BYTES>
 int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
            const uint64_t* idx, uint64_t n_idx, void* dst) {
-    using V = typename Vec<BYTES>::T;
     static const uint32_t chunk = getenv("SYNK_GATHER_ROWS") ? atoi(getenv("SYNK_GATHER_ROWS")) : 4;
     // At most 8 CTAs of 8 warps per SM (about 2.7 waves at 3 resident
     // CTAs/SM: the oversubscription balances the random-row latency).
+    // 4 rows x 2 vectors in flight per lane at <= 85 registers (3 CTAs/SM) won
+    // the sweep (profiles/r01_gather.md): (4,1)x4 CTAs 0.77, (8,1)x2 0.57,
+    // (2,4)x3 0.91 with a slower e2e, (8,2)x1 0.55, (2,2)x4 0.88 of HBM.
     const uint64_t chunks = (n_idx + chunk - 1) / chunk;
     uint64_t blocks = (chunks * 32 + kBlock - 1) / kBlock;
     const uint64_t cap = (uint64_t)d->num_sms * 8;
     if (blocks > cap) blocks = cap;
-    gather_rows_kernel<BYTES><<<(unsigned)blocks, kBlock, 0, d->stream>>>(
-        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, chunk, (V*)dst, d->err_dev);
+    launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
     SYNK_LAUNCHED("gather_rows_kernel");
     return SYNK_OK;
 }
