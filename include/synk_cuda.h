@@ -96,6 +96,16 @@ int synk_mark_elapsed(synk_dev* dev, int a, int b, double* seconds);
  * phase barrier between sgd.cpp:301 and :314 of the reference). */
 int synk_signal(synk_dev* dev);
 int synk_wait_peer(synk_dev* dev, const synk_dev* peer);
+/* The same with one of 64 independent signal slots per rank (e.g. one per
+ * gradient segment, so each segment's all-reduce + update can start as soon
+ * as every rank finished that segment). */
+int synk_signal_slot(synk_dev* dev, int slot);
+int synk_wait_peer_slot(synk_dev* dev, const synk_dev* peer, int slot);
+/* A second context of the same rank and GPU with its own stream (and marks,
+ * flags): collectives overlapped with the rank's compute stream (bucketed
+ * gradient all-reduce + update during the backward pass, sgd.cpp:301-319).
+ * Closed with synk_close. */
+int synk_open_aux(synk_dev* main, synk_dev** aux);
 int synk_mark_reset(synk_dev* dev);
 
 /* ---- memory ------------------------------------------------------------------ */
@@ -264,6 +274,14 @@ int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, u
 int synk_mlp_loss_grad(synk_dev* dev, int dtype, const uint64_t* dims, uint32_t layers,
                        const void* params, const void* x, const void* y, uint64_t n,
                        double* loss_dev, void* grad, void* workspace, uint64_t workspace_bytes);
+/* synk_mlp_loss_grad_ex that, for the bf16 tensor-core path, records
+ * synk_signal_slot(dev, signal_base + l) as soon as the gradient segment of
+ * layer l ([W_l, b_l] in the flat layout) is final; *signalled = the number
+ * of segments signalled (0: nothing signalled, e.g. the native path). */
+int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                           const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
+                           void* grad, void* workspace, uint64_t workspace_bytes, int signal_base,
+                           int* signalled);
 /* Same with a compute mode: SYNK_MLP_NATIVE runs every product in the
  * parameter dtype on the CUDA cores (f32 FFMA / f64 DFMA); SYNK_MLP_BF16_TC
  * (f32 parameters only) runs every dense product on tcgen05 tensor cores

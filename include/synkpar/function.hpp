@@ -56,6 +56,15 @@ struct UpdateDelta {
     UpdateCombine combine = UpdateCombine::Add;
 };
 
+// A span of the flat gradient a device kernel reports final (and whose
+// parameters it no longer reads) while its work is still in flight: it
+// recorded synk_signal_slot(ctx.dev, slot) right after the producing launch.
+struct GradSegment {
+    std::size_t first = 0;
+    std::size_t count = 0;
+    int slot = -1;
+};
+
 struct KernelContext {
     std::size_t rank = 0;
     std::size_t world = 1;
@@ -74,6 +83,10 @@ struct KernelContext {
     const std::vector<DevBuffer>* device_replicas = nullptr;
     const DevBuffer& device_replica(std::size_t i) const;
     DevBuffer device_alloc(std::vector<std::size_t> shape, DType dtype) const;
+    // Overlapped trainer step: slots grad_signal_base + i are free for a
+    // kernel to signal gradient segments with; it reports them here.
+    int grad_signal_base = -1;
+    std::vector<GradSegment>* grad_segments = nullptr;
 };
 
 struct KernelResult {
@@ -152,9 +165,10 @@ class ParallelFunction;
 namespace detail {
 struct PhaseRendezvous;
 // Executor internal (the fused trainer step): call() plus work chained inside its phase.
+using CallTail = std::function<void(std::size_t rank, const std::vector<std::size_t>& eff_rows,
+                                   const std::vector<GradSegment>& segments)>;
 CallResult call_with_tail(const ParallelFunction& f, const std::vector<FunctionArg>& args, const CallOptions& opts,
-                          const std::function<void(std::size_t, const std::vector<std::size_t>&)>& tail,
-                          PhaseRendezvous* rv);
+                          const CallTail& tail, PhaseRendezvous* rv, int grad_signal_base = -1);
 } // namespace detail
 
 class ParallelFunction {
@@ -177,9 +191,8 @@ private:
                                      std::vector<UpdateSpec>);
     friend void distribute(WorkerPool&);
     friend CallResult detail::call_with_tail(const ParallelFunction&, const std::vector<FunctionArg>&,
-                                             const CallOptions&,
-                                             const std::function<void(std::size_t, const std::vector<std::size_t>&)>&,
-                                             detail::PhaseRendezvous*);
+                                             const CallOptions&, const detail::CallTail&, detail::PhaseRendezvous*,
+                                             int);
     explicit ParallelFunction(std::shared_ptr<detail::FunctionCore> core) : core_(std::move(core)) {}
     std::shared_ptr<detail::FunctionCore> core_;
 };

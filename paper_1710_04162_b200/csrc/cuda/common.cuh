@@ -24,7 +24,7 @@ struct synk_dev {
     volatile int* err_host = nullptr;
     int* err_dev = nullptr;
     std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
-    cudaEvent_t ready = nullptr;     // synk_signal point (no timing), waited on by peers' streams
+    cudaEvent_t ready[64] = {};      // synk_signal_slot points (no timing), waited on by peers' streams
     void* graphs = nullptr;          // CUDA-graph cache of the MLP loss/grad launch sequence (mlp.cu)
     int marks_used = 0;
 };

@@ -406,7 +406,7 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
 }
 
 int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P, const float* theta, const float* x,
-                   const float* y, uint64_t n, double* loss, float* grad, void* ws) {
+                   const float* y, uint64_t n, double* loss, float* grad, void* ws, int signal_base = -1) {
     Bf16Plan B = make_bf16_plan(dims, L, n, P.maxd);
     char* base = static_cast<char*>(ws);
     auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
@@ -474,6 +474,11 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
                                    SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr, nullptr, 0);
             rc)
             return rc;
+        // Segment [W_l, b_l] of the gradient is final, and the f32 W_l/b_l are
+        // not read again in this pass (the GEMMs read the bf16 copies made at
+        // the start): the trainer may all-reduce + update it from here on.
+        if (signal_base >= 0)
+            if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
         if (l > 0) {
             // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
             const int nxt = cur ^ 1;
@@ -618,6 +623,27 @@ int synk_mlp_loss_grad_ex(synk_dev* d, int dtype, int compute, const uint64_t* d
     synk::DeviceGuard g(d->device);
     return loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n, loss_dev,
                           (float*)grad, workspace);
+}
+
+int synk_mlp_loss_grad_seg(synk_dev* d, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                           const void* params, const void* x, const void* y, uint64_t n, double* loss_dev, void* grad,
+                           void* workspace, uint64_t workspace_bytes, int signal_base, int* signalled) {
+    *signalled = 0;
+    if (compute != SYNK_MLP_BF16_TC || signal_base < 0)
+        return synk_mlp_loss_grad_ex(d, dtype, compute, dims, layers, params, x, y, n, loss_dev, grad, workspace,
+                                     workspace_bytes);
+    SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
+    SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
+    SYNK_REQUIRE(signal_base + (int)layers <= 64, SYNK_EARG, "mlp_loss_grad_seg: signal slots out of range");
+    Plan p;
+    if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
+    SYNK_REQUIRE(workspace_bytes >= make_bf16_plan(dims, layers, n, p.maxd).total, SYNK_EARG,
+                 "mlp: workspace too small");
+    synk::DeviceGuard g(d->device);
+    const int rc = loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n,
+                                  loss_dev, (float*)grad, workspace, signal_base);
+    if (rc == SYNK_OK) *signalled = (int)layers;
+    return rc;
 }
 
 int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, uint64_t n,

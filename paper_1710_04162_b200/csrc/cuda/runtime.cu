@@ -149,7 +149,8 @@ int synk_close(synk_dev* d) {
     cudaFreeHost(d->flags_host);
     cudaFreeHost(const_cast<int*>(d->err_host));
     for (cudaEvent_t e : d->marks) cudaEventDestroy(e);
-    if (d->ready) cudaEventDestroy(d->ready);
+    for (cudaEvent_t e : d->ready)
+        if (e) cudaEventDestroy(e);
     release_graphs(d);
     delete d;
     return SYNK_OK;
@@ -186,17 +187,49 @@ int synk_mark(synk_dev* d, int* mark) {
     return SYNK_OK;
 }
 
-int synk_signal(synk_dev* d) {
+int synk_signal_slot(synk_dev* d, int slot) {
+    SYNK_REQUIRE(slot >= 0 && slot < 64, SYNK_EARG, "synk_signal_slot: slot out of range");
     DeviceGuard g(d->device);
-    if (!d->ready) SYNK_CU(cudaEventCreateWithFlags(&d->ready, cudaEventDisableTiming));
-    SYNK_CU(cudaEventRecord(d->ready, d->stream));
+    if (!d->ready[slot]) SYNK_CU(cudaEventCreateWithFlags(&d->ready[slot], cudaEventDisableTiming));
+    SYNK_CU(cudaEventRecord(d->ready[slot], d->stream));
     return SYNK_OK;
 }
 
-int synk_wait_peer(synk_dev* d, const synk_dev* peer) {
-    SYNK_REQUIRE(peer && peer->ready, SYNK_EARG, "synk_wait_peer: the peer has not signalled");
+int synk_wait_peer_slot(synk_dev* d, const synk_dev* peer, int slot) {
+    SYNK_REQUIRE(slot >= 0 && slot < 64, SYNK_EARG, "synk_wait_peer_slot: slot out of range");
+    SYNK_REQUIRE(peer && peer->ready[slot], SYNK_EARG, "synk_wait_peer: the peer has not signalled");
     DeviceGuard g(d->device);
-    SYNK_CU(cudaStreamWaitEvent(d->stream, peer->ready, 0));
+    SYNK_CU(cudaStreamWaitEvent(d->stream, peer->ready[slot], 0));
+    return SYNK_OK;
+}
+
+int synk_signal(synk_dev* d) { return synk_signal_slot(d, 0); }
+
+int synk_wait_peer(synk_dev* d, const synk_dev* peer) { return synk_wait_peer_slot(d, peer, 0); }
+
+int synk_open_aux(synk_dev* main, synk_dev** out) {
+    *out = nullptr;
+    DeviceGuard g(main->device);
+    synk_dev* d = new synk_dev();
+    d->rank = main->rank;
+    d->device = main->device;
+    d->num_sms = main->num_sms;
+    cudaError_t e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&d->flags_dev, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(d->flags_dev, 0, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaHostAlloc(&d->flags_host, 4 * sizeof(int), cudaHostAllocPortable);
+    void* eh = nullptr;
+    if (e == cudaSuccess) e = cudaHostAlloc(&eh, 64, cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        std::memset(eh, 0, 64);
+        d->err_host = static_cast<volatile int*>(eh);
+        e = cudaHostGetDevicePointer((void**)&d->err_dev, eh, 0);
+    }
+    if (e != cudaSuccess) {
+        synk_close(d);
+        return cuda_fail(e, "synk_open_aux");
+    }
+    *out = d;
     return SYNK_OK;
 }
 

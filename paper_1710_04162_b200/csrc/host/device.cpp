@@ -26,7 +26,13 @@ void check(int rc, const char* what) {
     if (rc != SYNK_OK) throw_status(rc, what);
 }
 
+synk_dev* RankDevice::aux_handle() {
+    if (!aux) check(synk_open_aux(h, &aux), "open aux stream");
+    return aux;
+}
+
 RankDevice::~RankDevice() {
+    if (aux) synk_close(aux);
     if (staging) synk_host_free(staging);
     if (h && scratch) synk_free(h, scratch);
     if (h) synk_close(h);

@@ -42,6 +42,10 @@ struct RankDevice {
     static constexpr std::size_t kStagingBytes = std::size_t(64) << 10;
     void* staging = nullptr;
     std::mutex staging_mu;
+    // Second stream of this rank (synk_open_aux), opened on first use: the
+    // trainer's per-segment all-reduce + update overlapping the backward pass.
+    synk_dev* aux = nullptr;
+    synk_dev* aux_handle();
     ~RankDevice();
 };
 

@@ -74,7 +74,8 @@ DevBuffer as_dtype(const std::shared_ptr<detail::RankDevice>& rd, const DevBuffe
 // Enqueue loss + gradient on rd's stream. Returns (loss f64 scalar, grad).
 std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::RankDevice>& rd, const Checked& c,
                                                  const DevBuffer& params, const DevBuffer& x, const DevBuffer& y,
-                                                 MlpCompute compute = MlpCompute::Native) {
+                                                 MlpCompute compute = MlpCompute::Native,
+                                                 const KernelContext* ctx = nullptr) {
     const DType dt = params.dtype();
     if (compute == MlpCompute::Bf16TensorCore && dt != DType::Float32)
         throw DTypeError("mlp_grad_kernel: bf16 tensor-core compute needs float32 parameters");
@@ -87,9 +88,24 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     void* ws = detail::rank_scratch(rd, ws_bytes);
     DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
     DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
-    detail::check(synk_mlp_loss_grad_ex(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
-                                        yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws, ws_bytes),
+    const int base = ctx && ctx->grad_segments ? ctx->grad_signal_base : -1;
+    int signalled = 0;
+    detail::check(synk_mlp_loss_grad_seg(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
+                                         yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws, ws_bytes,
+                                         base, &signalled),
                   "mlp_loss_grad");
+    if (signalled > 0) {
+        // Layer l's segment [W_l, b_l] was signalled on slot base + l, in
+        // backward order (l = L-1 ... 0); W_l and b_l are adjacent in the layout.
+        std::size_t at = 0;
+        std::vector<std::size_t> first(L), count(L);
+        for (std::uint32_t l = 0; l < L; ++l) {
+            first[l] = at;
+            count[l] = c.dims[l] * c.dims[l + 1] + c.dims[l + 1];
+            at += count[l];
+        }
+        for (std::uint32_t l = L; l-- > 0;) ctx->grad_segments->push_back({first[l], count[l], base + int(l)});
+    }
     return {loss, grad};
 }
 
@@ -167,7 +183,7 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
     k.device_fn = [segs, grads_id, compute](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
         const DevBuffer& params = ctx.device_replica(0);
         Checked c = check_operands(params, segs, in[0], in[1]);
-        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute);
+        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute, &ctx);
         DeviceKernelResult r;
         r.outputs.push_back(loss);
         r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});

@@ -209,49 +209,100 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     const std::uint64_t t_next = t_ + 1;
     const bool timing = call_opts.device_timing;
     int ma = -1, mb = -1;
+    bool aux_marks = false;  // the update ran on rank 0's second stream (overlapped)
     detail::PhaseRendezvous rv(W);
 
-    auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows) {
+    // Overlap: a kernel that reports gradient segments as they become final
+    // (the bf16 MLP: one per layer, in backward order) gets each segment's
+    // all-reduce + update on the rank's second stream as soon as every rank
+    // signalled it -- the DDP-style bucketed overlap of the collective with
+    // the rest of the backward pass. Used only when every rank reported the
+    // same full cover of the gradient and no unequal-shard pre-scale is due.
+    constexpr int kSegBase = 1, kAuxDone = 63;
+    std::vector<std::size_t> seg_counts(W, 0);
+    std::vector<char> seg_cover(W, 0);
+    const std::size_t n_total = grads[0].size();
+
+    auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows, const std::vector<GradSegment>& segs) {
         const auto& rd = st->ranks[r];
         const int dt = detail::synk_dtype(grads[r].dtype());
+        std::size_t total = 0;
+        bool unequal = false;
         if (opts_.grad_op == ReduceOp::Mean && W > 1) {
-            // Unequal shards: pre-scale each rank's shard-mean gradient by
-            // rows_r*W/total so the equal-weight mean is the global row mean.
-            std::size_t total = 0;
-            bool unequal = false;
             for (std::size_t x : rows) total += x;
             for (std::size_t x : rows) unequal |= x * W != total;
-            if (unequal && total > 0)
-                detail::check(synk_scale(rd->h, dt, grads[r].data(), double(rows[r]) * double(W) / double(total),
-                                         grads[r].size()),
-                              "unequal-shard pre-scale");
+            unequal = unequal && total > 0;
+        }
+        std::size_t covered = 0;
+        for (const GradSegment& g : segs) covered += g.count;
+        seg_counts[r] = segs.size();
+        seg_cover[r] = !segs.empty() && covered == n_total;
+        if (unequal) {
+            // Unequal shards: pre-scale each rank's shard-mean gradient by
+            // rows_r*W/total so the equal-weight mean is the global row mean.
+            detail::check(synk_scale(rd->h, dt, grads[r].data(), double(rows[r]) * double(W) / double(total),
+                                     grads[r].size()),
+                          "unequal-shard pre-scale");
         }
         if (W > 1) {
             detail::check(synk_signal(rd->h), "signal");
             rv.arrive_and_wait();
-            for (std::size_t p = 0; p < W; ++p)
-                if (p != r) detail::check(synk_wait_peer(rd->h, st->handles[p]), "wait peer");
         }
+        bool overlap = !unequal;
+        for (std::size_t p = 0; p < W; ++p) overlap = overlap && seg_cover[p] && seg_counts[p] == segs.size();
         // The gradient update may have swapped each rank's grads replica for a
         // fresh buffer (WeightedMeanByRows adopts its accumulator): read the
         // pointers only now, after every rank applied its update.
         std::vector<void*> gp(W);
         for (std::size_t p = 0; p < W; ++p) gp[p] = grads[p].data();
-        if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
-        detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
-                                           hyper.data(), lr_, t_next, pp.data(), gp.data(),
-                                           a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
-                                           grads[r].size(), coherent ? 1 : 0),
-                      "fused all-reduce + update");
-        if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
+        if (!overlap) {
+            for (std::size_t p = 0; p < W && W > 1; ++p)
+                if (p != r) detail::check(synk_wait_peer(rd->h, st->handles[p]), "wait peer");
+            if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
+            detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
+                                               hyper.data(), lr_, t_next, pp.data(), gp.data(),
+                                               a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
+                                               grads[r].size(), coherent ? 1 : 0),
+                          "fused all-reduce + update");
+            if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
+            return;
+        }
+        synk_dev* aux = rd->aux_handle();
+        if (r == 0 && timing) {
+            detail::check(synk_mark_reset(aux), "marks");
+            aux_marks = true;
+        }
+        const std::size_t es = dtype_size(grads[r].dtype());
+        auto at = [es](const std::vector<void*>& v, std::size_t first) {
+            std::vector<void*> o(v.size());
+            for (std::size_t i = 0; i < v.size(); ++i) o[i] = v[i] ? static_cast<char*>(v[i]) + first * es : nullptr;
+            return o;
+        };
+        for (std::size_t k = 0; k < segs.size(); ++k) {
+            const GradSegment& g = segs[k];
+            for (std::size_t p = 0; p < W; ++p)  // every rank (this one included) finished this segment
+                detail::check(synk_wait_peer_slot(aux, st->handles[p], g.slot), "wait segment");
+            if (r == 0 && timing && k == 0) detail::check(synk_mark(aux, &ma), "mark");
+            std::vector<void*> ps = at(pp, g.first), gs = at(gp, g.first), x0 = at(a0, g.first), x1 = at(a1, g.first);
+            detail::check(synk_all_reduce_step(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
+                                               hyper.data(), lr_, t_next, ps.data(), gs.data(),
+                                               a0.empty() ? nullptr : x0.data(), a1.empty() ? nullptr : x1.data(),
+                                               g.count, coherent ? 1 : 0),
+                          "segment all-reduce + update");
+        }
+        if (r == 0 && timing) detail::check(synk_mark(aux, &mb), "mark");
+        // Join: the rank's own stream (whose synchronisation ends the phase)
+        // waits for the overlapped updates.
+        detail::check(synk_signal_slot(aux, kAuxDone), "signal aux");
+        detail::check(synk_wait_peer_slot(rd->h, aux, kAuxDone), "join aux");
     };
-    CallResult gr = detail::call_with_tail(f_grad, batch, call_opts, tail, &rv);
+    CallResult gr = detail::call_with_tail(f_grad, batch, call_opts, tail, &rv, kSegBase);
     if (gr.outputs.empty()) throw ArgumentError("train_step(): gradient function must output the loss");
     const double loss = gr.outputs[0].get(0);
     rep.grad_call = gr.report;
     if (ma >= 0 && mb >= 0) {
         double sec = 0.0;
-        detail::check(synk_mark_elapsed(st->ranks[0]->h, ma, mb, &sec), "timing");
+        detail::check(synk_mark_elapsed(aux_marks ? st->ranks[0]->aux : st->ranks[0]->h, ma, mb, &sec), "timing");
         rep.allreduce_s = sec;
         rep.step_call.total_s = sec;
     }

@@ -298,3 +298,29 @@ def test_c5_full_size_bf16_gradient_vs_fp64(sk, oracle):
         trainer = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
         trainer.train_step(f, [x, y])
         assert block.params.get(0).tobytes() == oracle.sgd(p0, block.grads.get(0), 0.01).tobytes()
+
+
+@pytest.mark.parametrize("world,rule", [(1, "sgd"), (2, "adam"), (3, "momentum")])
+def test_overlapped_segment_updates_bitwise(sk, world, rule):
+    """bf16 MLP through the Trainer: each layer's gradient segment is
+    all-reduced + applied on the rank's second stream as soon as every rank
+    finished it (overlapping the rest of the backward pass). Same arithmetic
+    per element as the non-overlapped step (check_finite=True keeps the
+    reference's two-phase sequence): parameters and optimizer state must
+    match bit for bit after several steps, replicas coherent."""
+    cfg = sk.MlpConfig(in_dim=256, width=384, out_dim=100, layers=3, seed=3)
+    x, y = sk.mlp_make_dataset(512 * world, cfg, seed=4, dtype="f32")
+    rules = {"sgd": sk.SgdRule, "adam": sk.AdamRule, "momentum": sk.MomentumRule}
+    params = {}
+    for check_finite in (False, True):
+        with sk.Pool(workers=world) as pool:
+            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+            f = sk.mlp_grad_function(pool, block, compute="bf16")
+            sk.distribute(pool)
+            tr = sk.Trainer(pool, block, rules[rule](), lr=1e-2, check_finite=check_finite, verify_coherence=True)
+            rng = np.random.default_rng(7)
+            for _ in range(4):
+                tr.train_step(f, [x, y], indexes=rng.integers(0, x.shape[0], 256 * world))
+            assert block.params.coherent
+            params[check_finite] = block.params.get(world - 1)
+    assert params[False].tobytes() == params[True].tobytes()
