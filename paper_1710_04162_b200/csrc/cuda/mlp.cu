@@ -106,10 +106,12 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(
 }
 
 // Fixed (device-independent, so results do not depend on the SM count) split
-// of K for f32 products with too few output tiles to fill the GPU: ~2 CTAs per
+// of K for f32 products with too few output tiles to fill the GPU: ~3 CTAs per
 // SM of a 148-SM B200, at least 32 k per split. f64 stays unsplit (its
 // trajectories are held to 1e-10 against the reference's sequential sums).
-constexpr int64_t kSplitTargetCtas = 296;
+// 3 CTAs of 256 threads per SM fit at 80 registers: one full wave (measured
+// on C1: 444 -> 127 us/step, 296 -> 131, 592 -> 133, 888 -> 134).
+constexpr int64_t kSplitTargetCtas = 444;
 
 inline int64_t split_k(int es, int64_t M, int64_t N, int64_t K, int64_t* kper) {
     const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
