@@ -613,3 +613,39 @@ def test_c4_full_scale_all_reduce_broadcast(sk):
         var.broadcast(0)
         assert var.get(1).tobytes() == b.tobytes()
         assert var.coherent
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_index_list_edge_cases(sk, world):
+    """Empty index list, a list shorter than the world (ranks with no rows),
+    all-duplicate indices, first/last rows, a RowRange, and 1-row / 3-byte-ish
+    ragged row sizes (4-byte and 8-byte vector paths): every result equals
+    numpy fancy indexing bit for bit; Sum over zero rows raises like the
+    reference (function.cpp:330-363)."""
+    rng = np.random.default_rng(13)
+    with sk.Pool(workers=world) as pool:
+        f = sk.make_function(pool, sk.identity_kernel(), ["scatter"], ["gather"])
+        cnt = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
+        sk.distribute(pool)
+        for shape, dt in (((1000, 7), np.float32), ((333, 1), np.float64), ((50, 3), np.float32)):
+            src = rng.uniform(-1, 1, shape).astype(dt)
+            arr = sk.SharedInput.from_array(src)
+            for mirror in (False, True):
+                if mirror:
+                    arr.mirror(pool)
+                for idx in (np.zeros(0, np.int64), np.array([shape[0] - 1]), np.full(17, 5),
+                            np.array([0, shape[0] - 1] * 3), rng.integers(0, shape[0], 1001)):
+                    pinned = sk.pinned_array(max(idx.size, 1), "int64")[: idx.size]
+                    pinned[:] = idx
+                    for sel in (idx, pinned):
+                        (got,) = f.call([arr], indexes=sel)
+                        # no rows anywhere: concat_rows of no parts is zeros({0}) (tensor.cpp:288)
+                        assert got.shape == ((idx.size,) + shape[1:] if idx.size else (0,))
+                        assert got.tobytes() == src[idx].tobytes()
+                    if idx.size == 0:
+                        with pytest.raises(sk.ArgumentError):
+                            cnt.call([arr], indexes=idx)
+                    else:
+                        assert float(cnt.call([arr], indexes=idx)[0]) == idx.size
+                (rg,) = f.call([arr], indexes=(3, min(40, shape[0])))
+                assert rg.tobytes() == src[3:min(40, shape[0])].tobytes()
