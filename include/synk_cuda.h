@@ -106,6 +106,14 @@ int synk_wait_peer_slot(synk_dev* dev, const synk_dev* peer, int slot);
  * gradient all-reduce + update during the backward pass, sgd.cpp:301-319).
  * Closed with synk_close. */
 int synk_open_aux(synk_dev* main, synk_dev** aux);
+/* Caller-owned timing events on dev's device (independent of the rank's mark
+ * ring, so they can be read long after later calls reused the marks): the
+ * trainer records its step's stage boundaries here and resolves the
+ * StepReport's device times only when the report is read. */
+int synk_timer_create(synk_dev* dev, int count, void** timer);
+int synk_timer_record(synk_dev* dev, void* timer, int i);
+int synk_timer_elapsed(void* timer, int a, int b, double* seconds);
+int synk_timer_destroy(void* timer);
 int synk_mark_reset(synk_dev* dev);
 
 /* ---- memory ------------------------------------------------------------------ */

@@ -168,7 +168,8 @@ struct PhaseRendezvous;
 using CallTail = std::function<void(std::size_t rank, const std::vector<std::size_t>& eff_rows,
                                    const std::vector<GradSegment>& segments)>;
 CallResult call_with_tail(const ParallelFunction& f, const std::vector<FunctionArg>& args, const CallOptions& opts,
-                          const CallTail& tail, PhaseRendezvous* rv, int grad_signal_base = -1);
+                          const CallTail& tail, PhaseRendezvous* rv, int grad_signal_base = -1,
+                          const std::vector<void*>* ext_timers = nullptr);
 } // namespace detail
 
 class ParallelFunction {
@@ -192,7 +193,7 @@ private:
     friend void distribute(WorkerPool&);
     friend CallResult detail::call_with_tail(const ParallelFunction&, const std::vector<FunctionArg>&,
                                              const CallOptions&, const detail::CallTail&, detail::PhaseRendezvous*,
-                                             int);
+                                             int, const std::vector<void*>*);
     explicit ParallelFunction(std::shared_ptr<detail::FunctionCore> core) : core_(std::move(core)) {}
     std::shared_ptr<detail::FunctionCore> core_;
 };

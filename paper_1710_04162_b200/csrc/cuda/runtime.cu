@@ -207,6 +207,59 @@ int synk_signal(synk_dev* d) { return synk_signal_slot(d, 0); }
 
 int synk_wait_peer(synk_dev* d, const synk_dev* peer) { return synk_wait_peer_slot(d, peer, 0); }
 
+struct synk_timer_t {
+    int device = 0;
+    std::vector<cudaEvent_t> ev;
+};
+
+int synk_timer_create(synk_dev* d, int count, void** out) {
+    *out = nullptr;
+    SYNK_REQUIRE(count > 0 && count <= 64, SYNK_EARG, "synk_timer_create: 1..64 events");
+    DeviceGuard g(d->device);
+    auto* t = new synk_timer_t();
+    t->device = d->device;
+    for (int i = 0; i < count; ++i) {
+        cudaEvent_t e = nullptr;
+        cudaError_t err = cudaEventCreate(&e);
+        if (err != cudaSuccess) {
+            synk_timer_destroy(t);
+            return cuda_fail(err, "synk_timer_create");
+        }
+        t->ev.push_back(e);
+    }
+    *out = t;
+    return SYNK_OK;
+}
+
+int synk_timer_record(synk_dev* d, void* timer, int i) {
+    auto* t = static_cast<synk_timer_t*>(timer);
+    SYNK_REQUIRE(t && i >= 0 && i < (int)t->ev.size() && t->device == d->device, SYNK_EARG,
+                 "synk_timer_record: bad timer/event");
+    DeviceGuard g(d->device);
+    SYNK_CU(cudaEventRecord(t->ev[i], d->stream));
+    return SYNK_OK;
+}
+
+int synk_timer_elapsed(void* timer, int a, int b, double* seconds) {
+    auto* t = static_cast<synk_timer_t*>(timer);
+    SYNK_REQUIRE(t && a >= 0 && b >= 0 && a < (int)t->ev.size() && b < (int)t->ev.size(), SYNK_EARG,
+                 "synk_timer_elapsed: bad event");
+    DeviceGuard g(t->device);
+    float ms = 0.f;
+    SYNK_CU(cudaEventElapsedTime(&ms, t->ev[a], t->ev[b]));
+    *seconds = ms * 1e-3;
+    return SYNK_OK;
+}
+
+int synk_timer_destroy(void* timer) {
+    auto* t = static_cast<synk_timer_t*>(timer);
+    if (!t) return SYNK_OK;
+    DeviceGuard g(t->device);
+    for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
+    delete t;
+    return SYNK_OK;
+}
+
 int synk_open_aux(synk_dev* main, synk_dev** out) {
     *out = nullptr;
     DeviceGuard g(main->device);

@@ -181,6 +181,39 @@ SyncSgd::SyncSgd(WorkerPool& pool, FlatParamBlock block, UpdateRule rule, double
 // the fused all-reduce + 1/W + update kernel; the phase-exit synchronisation
 // covers both. Same arithmetic, same order as the two-phase path (sgd.cpp:
 // 292-319 of the reference), without the host round trip between them.
+// Per-rank timing events of the fused step: 0..3 the gradient call (share
+// start, inputs staged, compute start, compute end), 4..5 rank 0's update.
+struct SyncSgd::StepTimers {
+    std::vector<void*> per_rank;
+    explicit StepTimers(const detail::PoolState& st) {
+        per_rank.assign(st.world, nullptr);
+        for (std::size_t r = 0; r < st.world; ++r)
+            detail::check(synk_timer_create(st.handles[r], 6, &per_rank[r]), "step timers");
+    }
+    ~StepTimers() {
+        for (void* t : per_rank) synk_timer_destroy(t);
+    }
+};
+
+const StepReport& SyncSgd::last_report() const {
+    if (report_pending_ && timers_) {
+        report_pending_ = false;
+        const auto& t = timers_->per_rank;
+        double scatter = 0.0, sec = 0.0;
+        last_.grad_call.rank_compute_s.assign(t.size(), 0.0);
+        for (std::size_t r = 0; r < t.size(); ++r) {
+            if (synk_timer_elapsed(t[r], 0, 1, &sec) == SYNK_OK) scatter += sec;
+            if (synk_timer_elapsed(t[r], 2, 3, &sec) == SYNK_OK) last_.grad_call.rank_compute_s[r] = sec;
+        }
+        last_.grad_call.scatter_s = scatter / double(t.size());
+        if (!t.empty() && synk_timer_elapsed(t[0], 4, 5, &sec) == SYNK_OK) {
+            last_.allreduce_s = sec;
+            last_.step_call.total_s = sec;
+        }
+    }
+    return last_;
+}
+
 double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<FunctionArg>& batch,
                            const CallOptions& call_opts, Clock::time_point t0) {
     StepReport rep;
@@ -207,7 +240,11 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     const std::vector<double> hyper = rule_hyper(rule_);
     const int code = rule_code(rule_);
     const std::uint64_t t_next = t_ + 1;
-    const bool timing = call_opts.device_timing;
+    // Device times go to the trainer's own timers, resolved on report access.
+    const bool lazy = call_opts.device_timing && call_opts.num_slices == 1;
+    const bool timing = call_opts.device_timing && !lazy;
+    if (lazy && (!timers_ || timers_->per_rank.size() != W)) timers_ = std::make_shared<StepTimers>(*st);
+    void* t0_timer = lazy ? timers_->per_rank[0] : nullptr;
     int ma = -1, mb = -1;
     bool aux_marks = false;  // the update ran on rank 0's second stream (overlapped)
     detail::PhaseRendezvous rv(W);
@@ -259,12 +296,14 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             for (std::size_t p = 0; p < W && W > 1; ++p)
                 if (p != r) detail::check(synk_wait_peer(rd->h, st->handles[p]), "wait peer");
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
+            if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
             detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                hyper.data(), lr_, t_next, pp.data(), gp.data(),
                                                a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
                                                grads[r].size(), coherent ? 1 : 0),
                           "fused all-reduce + update");
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
+            if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 5), "timer");
             return;
         }
         synk_dev* aux = rd->aux_handle();
@@ -283,6 +322,7 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             for (std::size_t p = 0; p < W; ++p)  // every rank (this one included) finished this segment
                 detail::check(synk_wait_peer_slot(aux, st->handles[p], g.slot), "wait segment");
             if (r == 0 && timing && k == 0) detail::check(synk_mark(aux, &ma), "mark");
+            if (r == 0 && t0_timer && k == 0) detail::check(synk_timer_record(aux, t0_timer, 4), "timer");
             std::vector<void*> ps = at(pp, g.first), gs = at(gp, g.first), x0 = at(a0, g.first), x1 = at(a1, g.first);
             detail::check(synk_all_reduce_step(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                hyper.data(), lr_, t_next, ps.data(), gs.data(),
@@ -291,12 +331,16 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
                           "segment all-reduce + update");
         }
         if (r == 0 && timing) detail::check(synk_mark(aux, &mb), "mark");
+        if (r == 0 && t0_timer) detail::check(synk_timer_record(aux, t0_timer, 5), "timer");
         // Join: the rank's own stream (whose synchronisation ends the phase)
         // waits for the overlapped updates.
         detail::check(synk_signal_slot(aux, kAuxDone), "signal aux");
         detail::check(synk_wait_peer_slot(rd->h, aux, kAuxDone), "join aux");
     };
-    CallResult gr = detail::call_with_tail(f_grad, batch, call_opts, tail, &rv, kSegBase);
+    CallOptions co = call_opts;
+    co.device_timing = timing;
+    CallResult gr = detail::call_with_tail(f_grad, batch, co, tail, &rv, kSegBase,
+                                           lazy ? &timers_->per_rank : nullptr);
     if (gr.outputs.empty()) throw ArgumentError("train_step(): gradient function must output the loss");
     const double loss = gr.outputs[0].get(0);
     rep.grad_call = gr.report;
@@ -316,6 +360,7 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     rep.loss = loss;
     rep.total_s = since(t0);
     last_ = rep;
+    report_pending_ = lazy;
     return loss;
 }
 
@@ -429,6 +474,7 @@ double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<Fun
     rep.loss = loss;
     rep.total_s = since(t0);
     last_ = rep;
+    report_pending_ = false;
     return loss;
 }
 
