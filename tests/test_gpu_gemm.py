@@ -324,3 +324,28 @@ def test_overlapped_segment_updates_bitwise(sk, world, rule):
             assert block.params.coherent
             params[check_finite] = block.params.get(world - 1)
     assert params[False].tobytes() == params[True].tobytes()
+
+
+@pytest.mark.parametrize("world,rows,slices", [(3, 700, 1), (2, 512, 2)])
+def test_fused_step_fallbacks_bitwise(sk, world, rows, slices):
+    """Paths where the trainer cannot overlap the segment updates: unequal
+    shards (the rows_r*W/total pre-scale must precede the all-reduce) and
+    num_slices > 1 (per-slice invocations: no final segments, eager report
+    timing). Bitwise equal to the two-phase step; reports populated."""
+    cfg = sk.MlpConfig(in_dim=128, width=256, out_dim=100, layers=3, seed=5)
+    x, y = sk.mlp_make_dataset(rows, cfg, seed=6, dtype="f32")
+    params = {}
+    for check_finite in (False, True):
+        with sk.Pool(workers=world) as pool:
+            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+            f = sk.mlp_grad_function(pool, block, compute="bf16")
+            sk.distribute(pool)
+            tr = sk.Trainer(pool, block, sk.AdamRule(), lr=1e-2, check_finite=check_finite)
+            for _ in range(3):
+                tr.train_step(f, [x, y], num_slices=slices)
+            rep = tr.last_report
+            assert rep["grad_call"]["rank_rows"] == [len(p) for p in np.array_split(np.arange(rows), world)]
+            assert max(rep["grad_call"]["rank_compute_s"]) > 0 and rep["allreduce_s"] > 0
+            assert block.params.coherent
+            params[check_finite] = block.params.get(0)
+    assert params[False].tobytes() == params[True].tobytes()
