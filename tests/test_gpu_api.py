@@ -111,7 +111,7 @@ def test_trainer_loss_decreases(sk):
 
 # ---- device built-in kernels: gather / slicing / aggregation -------------------------
 
-@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 def test_indexed_gather_bit_exact(sk, oracle, world):
     rng = np.random.default_rng(world)
     src = rng.uniform(-1, 1, (5000, 256)).astype(np.float32)
@@ -226,7 +226,7 @@ def test_gather_golden_through_api(sk):
                 assert rng_.tobytes() == g["%s_w%d_range" % (tag, world)].tobytes()
 
 
-@pytest.mark.parametrize("world,slices", [(1, 1), (2, 4), (3, 4), (4, 5)])
+@pytest.mark.parametrize("world,slices", [(1, 1), (2, 4), (3, 4), (4, 5), (8, 3)])
 def test_slicing_aggregation_column_stats(sk, oracle, world, slices):
     rng = np.random.default_rng(11)
     x = rng.uniform(-1, 1, (4099, 1024)).astype(np.float32)

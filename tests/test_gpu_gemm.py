@@ -300,7 +300,7 @@ def test_c5_full_size_bf16_gradient_vs_fp64(sk, oracle):
         assert block.params.get(0).tobytes() == oracle.sgd(p0, block.grads.get(0), 0.01).tobytes()
 
 
-@pytest.mark.parametrize("world,rule", [(1, "sgd"), (2, "adam"), (3, "momentum")])
+@pytest.mark.parametrize("world,rule", [(1, "sgd"), (2, "adam"), (3, "momentum"), (8, "rmsprop")])
 def test_overlapped_segment_updates_bitwise(sk, world, rule):
     """bf16 MLP through the Trainer: each layer's gradient segment is
     all-reduced + applied on the rank's second stream as soon as every rank
@@ -310,7 +310,7 @@ def test_overlapped_segment_updates_bitwise(sk, world, rule):
     match bit for bit after several steps, replicas coherent."""
     cfg = sk.MlpConfig(in_dim=256, width=384, out_dim=100, layers=3, seed=3)
     x, y = sk.mlp_make_dataset(512 * world, cfg, seed=4, dtype="f32")
-    rules = {"sgd": sk.SgdRule, "adam": sk.AdamRule, "momentum": sk.MomentumRule}
+    rules = {"sgd": sk.SgdRule, "adam": sk.AdamRule, "momentum": sk.MomentumRule, "rmsprop": sk.RmsPropRule}
     params = {}
     for check_finite in (False, True):
         with sk.Pool(workers=world) as pool:
