@@ -181,8 +181,9 @@ SyncSgd::SyncSgd(WorkerPool& pool, FlatParamBlock block, UpdateRule rule, double
 // the fused all-reduce + 1/W + update kernel; the phase-exit synchronisation
 // covers both. Same arithmetic, same order as the two-phase path (sgd.cpp:
 // 292-319 of the reference), without the host round trip between them.
-// Per-rank timing events of the fused step: 0..3 the gradient call (share
-// start, inputs staged, compute start, compute end), 4..5 rank 0's update.
+// Per-rank timing events of the fused step: 0, 1, 3 the gradient call (share
+// start, inputs staged = compute start, compute end), 4..5 rank 0's update
+// (4 omitted at W = 1 without overlap: the update starts at event 3).
 struct SyncSgd::StepTimers {
     std::vector<void*> per_rank;
     explicit StepTimers(const detail::PoolState& st) {
@@ -203,10 +204,10 @@ const StepReport& SyncSgd::last_report() const {
         last_.grad_call.rank_compute_s.assign(t.size(), 0.0);
         for (std::size_t r = 0; r < t.size(); ++r) {
             if (synk_timer_elapsed(t[r], 0, 1, &sec) == SYNK_OK) scatter += sec;
-            if (synk_timer_elapsed(t[r], 2, 3, &sec) == SYNK_OK) last_.grad_call.rank_compute_s[r] = sec;
+            if (synk_timer_elapsed(t[r], 1, 3, &sec) == SYNK_OK) last_.grad_call.rank_compute_s[r] = sec;
         }
         last_.grad_call.scatter_s = scatter / double(t.size());
-        if (!t.empty() && synk_timer_elapsed(t[0], 4, 5, &sec) == SYNK_OK) {
+        if (!t.empty() && synk_timer_elapsed(t[0], update_from_compute_end_ ? 3 : 4, 5, &sec) == SYNK_OK) {
             last_.allreduce_s = sec;
             last_.step_call.total_s = sec;
         }
@@ -296,7 +297,9 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             for (std::size_t p = 0; p < W && W > 1; ++p)
                 if (p != r) detail::check(synk_wait_peer(rd->h, st->handles[p]), "wait peer");
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
-            if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
+            // W = 1: the update directly follows the compute end (event 3) on this stream
+            if (r == 0 && t0_timer && W > 1) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
+            if (r == 0) update_from_compute_end_ = W == 1;
             detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                hyper.data(), lr_, t_next, pp.data(), gp.data(),
                                                a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
@@ -323,6 +326,7 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
                 detail::check(synk_wait_peer_slot(aux, st->handles[p], g.slot), "wait segment");
             if (r == 0 && timing && k == 0) detail::check(synk_mark(aux, &ma), "mark");
             if (r == 0 && t0_timer && k == 0) detail::check(synk_timer_record(aux, t0_timer, 4), "timer");
+            if (r == 0 && k == 0) update_from_compute_end_ = false;
             std::vector<void*> ps = at(pp, g.first), gs = at(gp, g.first), x0 = at(a0, g.first), x1 = at(a1, g.first);
             detail::check(synk_all_reduce_step(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                hyper.data(), lr_, t_next, ps.data(), gs.data(),
