@@ -127,6 +127,9 @@ int synk_host_alloc(uint64_t bytes, void** out);
 int synk_host_free(void* ptr);
 /* 0 = pageable host, 1 = pinned/mapped host, 2 = device memory. */
 int synk_ptr_kind(const void* ptr, int* kind, int* device);
+/* The device-side address of page-locked host memory (what a kernel reading
+ * it in place must use); SYNK_EARG if `host` is not page-locked. */
+int synk_host_device_ptr(const void* host, const void** dev_ptr);
 /* Asynchronous copy in any direction (NdBuffer::clone, tensor.cpp:155-159). */
 int synk_copy(synk_dev* dev, void* dst, const void* src, uint64_t bytes);
 /* Strided 2-D copy: `rows` rows of `row_bytes`, pitches in bytes. */

@@ -345,6 +345,20 @@ int synk_ptr_kind(const void* p, int* kind, int* device) {
     return SYNK_OK;
 }
 
+int synk_host_device_ptr(const void* host, const void** dev_ptr) {
+    *dev_ptr = nullptr;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, host) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        return fail(SYNK_EARG, "synk_host_device_ptr: not page-locked host memory");
+    }
+    // devicePointer is the address kernels use (equal to `host` for
+    // cudaHostAlloc'd memory under unified addressing; may differ for
+    // cudaHostRegister'd ranges on systems without host-pointer access).
+    *dev_ptr = attr.devicePointer ? attr.devicePointer : host;
+    return SYNK_OK;
+}
+
 int synk_copy(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
     if (bytes == 0) return SYNK_OK;
     DeviceGuard g(d->device);

@@ -48,9 +48,13 @@ void validate_view(const SelView& sel, std::size_t n) {
 
 namespace {
 
-bool is_mapped_host(const void* p) {
-    int kind = 0, dev = -1;
-    return p && synk_ptr_kind(p, &kind, &dev) == SYNK_OK && kind == 1;
+// Device-side address of page-locked host memory (kernels read it in place),
+// or nullptr when `host` is not page-locked.
+template <class T>
+const T* device_view(const T* host) {
+    const void* d = nullptr;
+    if (!host || synk_host_device_ptr(host, &d) != SYNK_OK) return nullptr;
+    return static_cast<const T*>(d);
 }
 
 } // namespace
@@ -87,8 +91,8 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     const std::pair<const std::uint64_t*, std::size_t> key{sel.list + part.start, part.count()};
     DevBuffer idx;
     const std::uint64_t* idx_ptr = nullptr;
-    if (is_mapped_host(key.first)) {
-        idx_ptr = key.first;  // pinned list: the gather kernel reads it in place over PCIe
+    if (const std::uint64_t* dv = device_view(key.first)) {
+        idx_ptr = dv;  // pinned list: the gather kernel reads it in place over PCIe
     } else {
         if (uploads)
             for (auto& [k, buf] : uploads->done)
@@ -104,8 +108,8 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     DevBuffer staged;  // keeps a device copy alive when the host source is pageable
     if (have_mirror) {
         base = static_cast<const char*>(mirror->data()) + src.offset_bytes();
-    } else if (is_mapped_host(src.bytes())) {
-        base = src.bytes();  // gather straight out of pinned host memory over PCIe
+    } else if (const std::byte* dv = device_view(src.bytes())) {
+        base = dv;  // gather straight out of pinned host memory over PCIe
     } else {
         staged = DevBuffer::alloc(rd, src.shape(), src.dtype());
         check(synk_copy(rd->h, staged.data(), src.bytes(), src.byte_size()), "excerpt: stage pageable source");

@@ -402,3 +402,26 @@ def test_mlp_loss_grad_vs_reference_golden(oracle):
         loss, grad = _mlp(R, g["params64"], [8, 16, 16, 16, 4], g["x64"], g["y64"], np.float64)
         assert oracle.elem_err(loss, float(g["loss64"])) <= 1e-12
         assert oracle.elem_err(grad, g["grad64"]) <= 1e-12
+
+
+def test_gather_from_host_registered_memory(sk, oracle):
+    """An index list in cudaHostRegister'd (page-locked, not cudaHostAlloc'd)
+    memory is borrowed in place and read by the gather kernel through its
+    device address (synk_host_device_ptr), bit-exact."""
+    import torch
+
+    rng = np.random.default_rng(8)
+    src = rng.uniform(-1, 1, (3000, 64)).astype(np.float32)
+    idx = rng.integers(0, 3000, 777).astype(np.int64)
+    cudart = torch.cuda.cudart()
+    for a in (src, idx):
+        assert int(cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)) == 0
+    try:
+        with sk.Pool(workers=2) as pool:
+            f = sk.make_function(pool, sk.identity_kernel(), ["scatter"], ["gather"])
+            sk.distribute(pool)
+            (got,) = f.call([src], indexes=idx)
+            assert got.tobytes() == oracle.gather_rows(src, idx.astype(np.uint64)).tobytes()
+    finally:
+        for a in (src, idx):
+            cudart.cudaHostUnregister(a.ctypes.data)
