@@ -286,34 +286,48 @@ def collectives_c4(sk, args, n_gpus):
     devices = [d % ndev for d in range(n_gpus)] if n_gpus >= 2 else [0, 0]
     sizes = [1 << k for k in range(10, 31, 3)] + [1 << 30]
     rng = np.random.default_rng(1000)
-    sweep = []
-    with sk.Pool(workers=world, devices=devices) as pool:
-        for S in sizes:
-            n = S // 4
-            var = sk.replicate(pool, np.zeros(n, np.float32))
-            for r in range(world):
-                var.set(r, rng.uniform(-1, 1, n).astype(np.float32))
-            reps = 200 if S <= (1 << 20) else (30 if S <= (1 << 27) else 8)
-            for _ in range(3):
-                var.all_reduce("mean")
-                var.broadcast(0)
-            t = time.perf_counter()
-            for _ in range(reps):
-                var.all_reduce("mean")
-            t_ar = (time.perf_counter() - t) / reps
-            t = time.perf_counter()
-            for _ in range(reps):
-                var.broadcast(0)
-            t_bc = (time.perf_counter() - t) / reps
-            coherent = var.coherent
-            del var
-            sweep.append({"bytes": S, "allreduce_us": 1e6 * t_ar, "allreduce_busbw_gbs": S / t_ar * 2 * (world - 1) / world / 1e9,
-                          "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9, "coherent": coherent})
+
+    def sweep_with(collectives):
+        sweep = []
+        with sk.Pool(workers=world, devices=devices, collectives=collectives) as pool:
+            for S in sizes:
+                n = S // 4
+                var = sk.replicate(pool, np.zeros(n, np.float32))
+                for r in range(world):
+                    var.set(r, rng.uniform(-1, 1, n).astype(np.float32))
+                reps = 200 if S <= (1 << 20) else (30 if S <= (1 << 27) else 8)
+                for _ in range(3):
+                    var.all_reduce("mean")
+                    var.broadcast(0)
+                t = time.perf_counter()
+                for _ in range(reps):
+                    var.all_reduce("mean")
+                t_ar = (time.perf_counter() - t) / reps
+                t = time.perf_counter()
+                for _ in range(reps):
+                    var.broadcast(0)
+                t_bc = (time.perf_counter() - t) / reps
+                coherent = var.coherent
+                del var
+                sweep.append({"bytes": S, "allreduce_us": 1e6 * t_ar,
+                              "allreduce_busbw_gbs": S / t_ar * 2 * (world - 1) / world / 1e9,
+                              "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9,
+                              "coherent": coherent})
+        return sweep
+
+    sweep = sweep_with("p2p")
     out = {"config": "C4: all_reduce mean + broadcast(0) of f32 buffers 1 KiB - 1 GiB, W=%d ranks" % world,
            "ranks": world, "devices": devices,
            "link": "NVLink peer memory" if len(set(devices)) >= 2 else "1 GPU: the ranks share it, peer-memory "
                                                                          "kernels run over local HBM (NVLink unmeasured)",
            "sweep": sweep}
+    # Library baseline on distinct GPUs: the same sweep through NCCL (busbw vs
+    # the NVLink peak, next to the peer-memory kernels above).
+    if len(set(devices)) >= 2 and sk.nccl_available():
+        try:
+            out["nccl_sweep"] = sweep_with("nccl")
+        except Exception as e:  # reported, not fatal
+            out["nccl_sweep"] = {"unavailable": str(e)[:200]}
     if not args.no_cpu_baseline:
         ref = []
         for S in (1 << 10, 1 << 16, 1 << 20, 1 << 26):

@@ -45,6 +45,7 @@ extern "C" {
 #define SYNK_ECUDA (-10)  /* CUDA runtime failure   */
 #define SYNK_ENOMEM (-11) /* allocation failure     */
 #define SYNK_ENODEV (-12) /* no usable CUDA device  */
+#define SYNK_ENCCL (-13)  /* NCCL failure (optional collectives backend) */
 
 #define SYNK_F32 1
 #define SYNK_F64 2
@@ -212,6 +213,19 @@ int synk_broadcast(synk_dev* dev, int world, int src, void* const* bufs, uint64_
  * replicated.cpp:115-137). */
 int synk_all_reduce_whole(synk_dev* dev, int world, int dtype, int op, void* const* bufs, uint64_t n);
 int synk_broadcast_whole(synk_dev* dev, int world, int src, void* const* bufs, uint64_t bytes);
+
+/* Optional NCCL backend (ForkOptions::collectives = "nccl"): the library
+ * baseline the peer-memory kernels are compared with on multi-GPU boxes.
+ * libnccl.so.2 is dlopen'ed on first use; one communicator per rank
+ * (ncclCommInitAll, distinct GPUs required), used from the rank's thread on
+ * its stream. Sum/mean results are NCCL's reduction order (within the
+ * reference's 8*W*eps tolerance, not its tree order); max/min/broadcast are
+ * exact. */
+int synk_nccl_available(void);
+int synk_nccl_open(int world, synk_dev* const* devs);
+int synk_nccl_close(synk_dev* dev);
+int synk_nccl_all_reduce(synk_dev* dev, int dtype, int op, void* buf, uint64_t n);
+int synk_nccl_broadcast(synk_dev* dev, int root, void* buf, uint64_t bytes);
 
 /* ---- optimizer ---------------------------------------------------------------- */
 /* hyper: momentum {mu}; rmsprop {rho, eps}; adam {beta1, beta2, eps}.

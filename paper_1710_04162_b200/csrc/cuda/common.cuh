@@ -26,6 +26,7 @@ struct synk_dev {
     std::vector<cudaEvent_t> marks;  // timing events, recycled by synk_mark_reset
     cudaEvent_t ready[64] = {};      // synk_signal_slot points (no timing), waited on by peers' streams
     void* graphs = nullptr;          // CUDA-graph cache of the MLP loss/grad launch sequence (mlp.cu)
+    void* nccl = nullptr;            // ncclComm_t of the optional NCCL backend (nccl_backend.cu)
     int marks_used = 0;
 };
 

@@ -152,6 +152,7 @@ int synk_close(synk_dev* d) {
     for (cudaEvent_t e : d->ready)
         if (e) cudaEventDestroy(e);
     release_graphs(d);
+    synk_nccl_close(d);
     delete d;
     return SYNK_OK;
 }

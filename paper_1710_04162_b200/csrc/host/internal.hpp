@@ -117,6 +117,7 @@ struct PoolState {
     // B200: rank r's GPU context.
     std::vector<std::shared_ptr<RankDevice>> ranks;
     std::vector<synk_dev*> handles;
+    bool nccl = false;  // ForkOptions::collectives == "nccl"
 };
 
 PhaseReport run_pool_phase(PoolState& st, PhaseKind kind, const std::function<void(std::size_t)>& work);

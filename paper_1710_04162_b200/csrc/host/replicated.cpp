@@ -120,6 +120,14 @@ void ReplicatedVariable::broadcast(std::size_t src) {
     }
     std::vector<void*> ptrs = replica_ptrs(rec);
     const std::size_t bytes = s.byte_size();
+    if (st.nccl) {  // library baseline backend (ForkOptions::collectives = "nccl")
+        detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+            detail::check(synk_nccl_broadcast(st.handles[r], static_cast<int>(src), ptrs[r], bytes), "broadcast (nccl)");
+            detail::dev_sync(st.ranks[r]);
+        });
+        rec.coherent = true;
+        return;
+    }
     if (bytes <= kWholeCollectiveBytes) {
         // Small buffer: rank 0's GPU copies every chunk over the peer pointers
         // (all streams are idle between phases), no rank thread is woken.
@@ -146,6 +154,15 @@ void ReplicatedVariable::all_reduce(ReduceOp op) {
     std::vector<void*> ptrs = replica_ptrs(rec);
     const std::size_t n = rec.replicas[0].size();
     const int dt = detail::synk_dtype(rec.replicas[0].dtype());
+    if (st.nccl) {  // library baseline backend: NCCL's reduction order (within tolerance, not bitwise)
+        detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+            require_same_dtype(rec);
+            detail::check(synk_nccl_all_reduce(st.handles[r], dt, detail::synk_op(op), ptrs[r], n), "all_reduce (nccl)");
+            detail::dev_sync(st.ranks[r]);
+        });
+        rec.coherent = true;
+        return;
+    }
     if (rec.replicas[0].byte_size() <= kWholeCollectiveBytes) {
         // Small buffer: one kernel on rank 0's GPU folds every chunk (same
         // per-element tree order) and writes all replicas over the peer

@@ -282,6 +282,24 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
                                      grads[r].size()),
                           "unequal-shard pre-scale");
         }
+        if (st->nccl) {
+            // Library baseline backend: NCCL all-reduce (sum, or avg = mean) of
+            // this rank's gradient in place, then the rule on the reduced
+            // gradient -- NCCL synchronises the ranks on the device.
+            if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
+            if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
+            if (r == 0) update_from_compute_end_ = false;
+            detail::check(synk_nccl_all_reduce(rd->h, dt, detail::synk_op(opts_.grad_op), grads[r].data(),
+                                               grads[r].size()),
+                          "gradient all-reduce (nccl)");
+            detail::check(synk_optimizer_step(rd->h, dt, code, hyper.data(), lr_, t_next, pp[r], grads[r].data(),
+                                              a0.empty() ? nullptr : a0[r], a1.empty() ? nullptr : a1[r],
+                                              grads[r].size()),
+                          "update (nccl path)");
+            if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
+            if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 5), "timer");
+            return;
+        }
         if (W > 1) {
             detail::check(synk_signal(rd->h), "signal");
             rv.arrive_and_wait();

@@ -649,3 +649,32 @@ def test_index_list_edge_cases(sk, world):
                         assert float(cnt.call([arr], indexes=idx)[0]) == idx.size
                 (rg,) = f.call([arr], indexes=(3, min(40, shape[0])))
                 assert rg.tobytes() == src[3:min(40, shape[0])].tobytes()
+
+
+def test_nccl_backend_optional(sk):
+    """The optional NCCL collectives backend (library baseline): on one GPU it
+    runs with one rank (identity all-reduce, the trainer's NCCL path), asks for
+    distinct GPUs otherwise, and rejects unknown backends."""
+    with pytest.raises(sk.ArgumentError):
+        sk.Pool(workers=1, collectives="mpi")
+    if not sk.nccl_available():
+        pytest.skip("libnccl.so.2 not loadable here")
+    if sk.device_count() < 2:
+        with pytest.raises(sk.ArgumentError, match="distinct GPU"):
+            sk.Pool(workers=2, devices=[0, 0], collectives="nccl")
+    rng = np.random.default_rng(2)
+    v = rng.standard_normal(1000)
+    with sk.Pool(workers=1, collectives="nccl") as pool:
+        var = sk.replicate(pool, v)
+        var.all_reduce("mean")
+        var.broadcast(0)
+        assert var.get(0).tobytes() == v.tobytes()
+        cfg = sk.MlpConfig(in_dim=16, width=32, out_dim=4, layers=2, seed=1)
+        x, y = sk.mlp_make_dataset(64, cfg, seed=3)
+        block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg))
+        f = sk.mlp_grad_function(pool, block)
+        sk.distribute(pool)
+        p0 = block.params.get(0)
+        sk.Trainer(pool, block, sk.SgdRule(), lr=0.1).train_step(f, [x, y])
+        g = block.grads.get(0)
+        np.testing.assert_allclose(block.params.get(0), p0 - 0.1 * g, rtol=0, atol=1e-15)
