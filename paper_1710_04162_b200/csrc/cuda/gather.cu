@@ -11,7 +11,10 @@
 // (then the same loads travel over PCIe). Out-of-range indices set the rank's
 // device error flag, reported as BoundsError at the phase-exit synk_sync().
 
+#include <cuda.h>
 #include <stdlib.h>
+
+#include <mutex>
 
 #include "common.cuh"
 
@@ -265,6 +268,155 @@ __global__ void __launch_bounds__(32) gather_rows_bulk_kernel(
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- TMA gather4 (cp.async.bulk.tensor ... tile::gather4) ------------------------
+//
+// Rows of 16..2048 bytes in device memory: one tensor-map request fetches FOUR
+// rows at arbitrary indices (Blackwell's gather4 mode) into shared memory --
+// a quarter of the per-row bulk requests, whose per-request cost capped the
+// per-row bulk kernel. Same pipeline: one warp per CTA, chunks of chunk_rows
+// (a multiple of 4) rows, an mbarrier per stage, one bulk store per landed
+// chunk (its rows are contiguous in dst), indices fetched two chunks ahead.
+// A bad index fetches row 0 (defined data) and sets the rank's error flag.
+// Measured (profiles/r01_gather.md): 0.913 of HBM at 2 CTAs/SM x 16-row
+// chunks vs 0.907-0.909 for the vector kernel -- the same random-row DRAM
+// ceiling reached through the TMA engine -- but slower end to end when the
+// index list is read over PCIe (one warp both fetches indices and issues), so
+// it stays opt-in (SYNK_GATHER_TMA4=1, device-resident sources only).
+
+__global__ void __launch_bounds__(32) gather_rows_tma4_kernel(
+    const __grid_constant__ CUtensorMap tmap, uint64_t src_rows, uint32_t row_bytes,
+    const uint64_t* __restrict__ idx, uint64_t n_idx, uint32_t chunk_rows, uint32_t stages, char* __restrict__ dst,
+    int* __restrict__ err) {
+    extern __shared__ __align__(128) char ring[];
+    __shared__ __align__(8) uint64_t full[kMaxStages];
+    const int lane = threadIdx.x;
+    const uint64_t n_chunks = (n_idx + chunk_rows - 1) / chunk_rows;
+    if (blockIdx.x >= n_chunks) return;
+    const uint64_t mine = (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const uint32_t stage_bytes = chunk_rows * row_bytes;
+    if (lane == 0) {
+        for (uint32_t s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    }
+    __syncwarp();
+
+    auto chunk_start = [&](uint64_t j) { return (blockIdx.x + j * gridDim.x) * (uint64_t)chunk_rows; };
+    auto load_index = [&](uint64_t j) -> uint64_t {
+        if (j >= mine) return 0;
+        const uint64_t r = chunk_start(j) + lane;
+        return lane < (int)chunk_rows && r < n_idx ? idx[r] : 0;
+    };
+    uint64_t q0 = load_index(0), q1 = load_index(1);
+
+    auto issue = [&](uint64_t j, uint64_t my) {
+        const uint32_t s = (uint32_t)(j % stages);
+        const uint64_t r0 = chunk_start(j);
+        const uint32_t cnt = (uint32_t)(n_idx - r0 < chunk_rows ? n_idx - r0 : chunk_rows);
+        const bool live = lane < (int)cnt;
+        const bool ok = live && my < src_rows;
+        if (live && !ok) *(volatile int*)err = 1;
+        const int row = ok ? (int)my : 0;  // rows past the chunk or bad: row 0 (fetched, never stored)
+        const uint32_t n_req = (cnt + 3) / 4;
+        const int q = lane & 7;
+        const int c0 = __shfl_sync(0xffffffffu, row, 4 * q), c1 = __shfl_sync(0xffffffffu, row, 4 * q + 1);
+        const int c2 = __shfl_sync(0xffffffffu, row, 4 * q + 2), c3 = __shfl_sync(0xffffffffu, row, 4 * q + 3);
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&full[s])),
+                         "r"(n_req * 4u * row_bytes)
+                         : "memory");
+        __syncwarp();
+        if (lane < (int)n_req) {
+            const uint32_t dst_s = smem_addr(ring + (size_t)s * stage_bytes + (size_t)lane * 4 * row_bytes);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst_s),
+                "l"(&tmap), "r"(smem_addr(&full[s])), "r"(0), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                : "memory");
+        }
+    };
+
+    const uint64_t ahead = stages - 2 < mine ? stages - 2 : mine;
+    for (uint64_t j = 0; j < ahead; ++j) {
+        issue(j, q0);
+        q0 = q1;
+        q1 = load_index(j + 2);
+    }
+    for (uint64_t j = 0; j < mine; ++j) {
+        const uint32_t s = (uint32_t)(j % stages);
+        bar_wait(smem_addr(&full[s]), (uint32_t)((j / stages) & 1));
+        const uint64_t r0 = chunk_start(j);
+        const uint32_t cnt = (uint32_t)(n_idx - r0 < chunk_rows ? n_idx - r0 : chunk_rows);
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + r0 * row_bytes),
+                         "r"(smem_addr(ring + (size_t)s * stage_bytes)), "r"(cnt * row_bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        const uint64_t jn = j + ahead;
+        if (jn < mine) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            issue(jn, q0);
+            q0 = q1;
+            q1 = load_index(jn + 2);
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn tiled_encoder() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+int launch_tma4(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes, const uint64_t* idx,
+                uint64_t n_idx, void* dst) {
+    EncodeTiledFn enc = tiled_encoder();
+    SYNK_REQUIRE(enc != nullptr, SYNK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {row_bytes / 8, src_rows};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)(row_bytes / 8), 1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<void*>(src), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SYNK_REQUIRE(r == CUDA_SUCCESS, SYNK_ECUDA, "cuTensorMapEncodeTiled (gather4) failed");
+    static const uint32_t ctas_per_sm = getenv("SYNK_TMA4_CTAS") ? atoi(getenv("SYNK_TMA4_CTAS")) : 2;
+    static const uint32_t max_chunk = getenv("SYNK_TMA4_CHUNK") ? atoi(getenv("SYNK_TMA4_CHUNK")) : 16;
+    const uint32_t budget = (224u * 1024u / ctas_per_sm - 1024u) & ~1023u;
+    uint32_t chunk_rows = max_chunk;
+    while (chunk_rows > 4 && (uint64_t)chunk_rows * row_bytes * 6 > budget) chunk_rows /= 2;
+    uint32_t stages = (uint32_t)(budget / (chunk_rows * row_bytes));
+    if (stages > kMaxStages) stages = kMaxStages;
+    if (stages < 3) return synk::fail(SYNK_EARG, "gather4: rows too wide for the ring");
+    const uint32_t smem = stages * chunk_rows * (uint32_t)row_bytes;
+    if (int rc = synk::ensure_max_smem((const void*)gather_rows_tma4_kernel, d->device, (int)(224u * 1024u)); rc)
+        return rc;
+    const uint64_t n_chunks = (n_idx + chunk_rows - 1) / chunk_rows;
+    const uint64_t cap = (uint64_t)d->num_sms * ctas_per_sm;
+    const unsigned grid = (unsigned)(n_chunks < cap ? n_chunks : cap);
+    gather_rows_tma4_kernel<<<grid, 32, smem, d->stream>>>(tmap, src_rows, (uint32_t)row_bytes, idx, n_idx,
+                                                           chunk_rows, stages, (char*)dst, d->err_dev);
+    SYNK_LAUNCHED("gather_rows_tma4_kernel");
+    return SYNK_OK;
+}
+
 int launch_bulk(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes, const uint64_t* idx,
                 uint64_t n_idx, void* dst) {
     static const uint32_t ctas_per_sm = getenv("SYNK_GATHER_CTAS") ? atoi(getenv("SYNK_GATHER_CTAS")) : 2;
@@ -299,6 +451,13 @@ extern "C" int synk_gather_rows(synk_dev* d, const void* src, uint64_t src_rows,
     // TMA cost) and on the C5 batch (8 KiB rows, 8192 rows: 32.8 vs 23.2 us);
     // it only won on very large 4 KiB-row launches (5,600 vs 5,494 GB/s).
     static const bool force_bulk = getenv("SYNK_GATHER_BULK") != nullptr;
+    static const bool use_tma4 = getenv("SYNK_GATHER_TMA4") != nullptr;  // A/B diagnostics (opt-in)
+    if (use_tma4 && (a & 15) == 0 && row_bytes <= 2048 && src_rows < (1ull << 31)) {
+        cudaPointerAttributes pa;
+        const bool on_device = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+        cudaGetLastError();
+        if (on_device) return launch_tma4(d, src, src_rows, row_bytes, idx, n_idx, dst);
+    }
     if (force_bulk && (a & 15) == 0 && row_bytes <= 8192)
         return launch_bulk(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 15) == 0) return launch<16>(d, src, src_rows, row_bytes, idx, n_idx, dst);

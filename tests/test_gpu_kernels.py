@@ -123,14 +123,16 @@ def test_gather_wide_rows(oracle, idx_in):
             assert R.sync() == 0
 
 
-def test_gather_bulk_kernel_subprocess():
-    """The opt-in cp.async.bulk (TMA engine) gather (SYNK_GATHER_BULK=1 is read
-    once per process): the wide-row and small-row parity tests in a child."""
+@pytest.mark.parametrize("variant", ["SYNK_GATHER_BULK", "SYNK_GATHER_TMA4"])
+def test_gather_bulk_kernel_subprocess(variant):
+    """The opt-in TMA gathers -- per-row cp.async.bulk (SYNK_GATHER_BULK=1) and
+    four-rows-per-request tensor-map gather4 (SYNK_GATHER_TMA4=1); both read
+    once per process -- through the gather parity tests in a child."""
     import os
     import subprocess
     import sys
 
-    env = dict(os.environ, SYNK_GATHER_BULK="1")
+    env = dict(os.environ, **{variant: "1"})
     here = os.path.dirname(os.path.abspath(__file__))
     out = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", os.path.join(here, "test_gpu_kernels.py"),
                           "-k", "gather and not subprocess"], env=env, capture_output=True, text=True, timeout=600,
