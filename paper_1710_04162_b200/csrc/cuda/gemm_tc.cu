@@ -884,6 +884,23 @@ __global__ void __launch_bounds__(256) prep2_bf16_kernel(const float* __restrict
     }
 }
 
+// Row-major bf16 cast only (no transpose): 8 consecutive elements per thread
+// (two 16-byte loads, one 16-byte store), grid-stride over rows x 8-column
+// groups; streaming loads (each f32 is read once).
+__global__ void __launch_bounds__(256) cast_bf16_rows_kernel(const float* __restrict__ in, uint64_t rows,
+                                                             uint64_t cols, uint64_t ld_in,
+                                                             __nv_bfloat16* __restrict__ out, uint64_t ld_out) {
+    const uint64_t groups = cols / 8, total = rows * groups;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
+        const uint64_t r = i / groups, c = (i - r * groups) * 8;
+        const float4* src = reinterpret_cast<const float4*>(in + r * ld_in + c);
+        const float4 a = __ldcs(src), b = __ldcs(src + 1);
+        __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                               __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+        *reinterpret_cast<uint4*>(out + r * ld_out + c) = *reinterpret_cast<const uint4*>(h);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -892,6 +909,16 @@ int synk_gemm_prep2_bf16(synk_dev* d, const float* in, uint64_t rows, uint64_t c
                          uint64_t ld_out, void* out_t, uint64_t ld_out_t) {
     if (rows == 0 || cols == 0 || (!out && !out_t)) return SYNK_OK;
     synk::DeviceGuard g(d->device);
+    if (!out_t && cols % 8 == 0 && ld_in % 4 == 0 && ld_out % 8 == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+        ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+        // cast only: the vectorised streaming kernel (no shared-memory tile)
+        const uint64_t total = rows * (cols / 8);
+        const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, (uint64_t)d->num_sms * 8);
+        cast_bf16_rows_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out),
+                                                           ld_out);
+        SYNK_LAUNCHED("cast_bf16_rows_kernel");
+        return SYNK_OK;
+    }
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
     const int vec_in = (ld_in % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
     prep2_bf16_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out), ld_out,
