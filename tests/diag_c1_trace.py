@@ -12,6 +12,7 @@ sys.path.insert(0, ".")
 import paper_1710_04162_b200 as sk  # noqa: E402
 
 world = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+per_rank = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 cfg = sk.MlpConfig(in_dim=784, width=512, out_dim=10, layers=2, seed=1)
 x, y = sk.mlp_make_dataset(65536, cfg, seed=2, dtype="f32")
 rng = np.random.default_rng(0)
@@ -29,7 +30,7 @@ with sk.Pool(workers=world) as pool:
         b[:] = rng.integers(0, 65536, n)
         return b
 
-    sel = [pinned(256 * world) for _ in range(400)]
+    sel = [pinned(per_rank * world) for _ in range(400)]
     for s in range(50):
         tr.train_step(g, [sx, sy], indexes=sel[s])
     t0 = time.perf_counter()
