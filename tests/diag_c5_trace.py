@@ -73,3 +73,16 @@ with sk.Pool(workers=1) as pool:
         a[2] = max(a[2], e.cpu_time_total)
     for k, (c, t, m) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:12]:
         print("cpu %-40s n=%5d total %10.1f us  max %10.1f us" % (k[:40], c, t, m))
+    # host runtime calls around the last step boundary (offsets vs the last device kernel of the step before)
+    allev = sorted(prof.events(), key=lambda e: e.time_range.start)
+    cu = [e for e in allev if e.device_type.name == "CPU" and e.name.startswith("cuda")]
+    ks_end = [e for e in ks if "copy_small" in e.name]
+    if len(ks_end) >= 2:
+        t_b = ks_end[-2].time_range.end
+        print("---- runtime calls within 120 us after the previous step's last kernel ----")
+        for e in cu:
+            if t_b - 60 <= e.time_range.start <= t_b + 120:
+                print("%8.1f %6.1f %s" % (e.time_range.start - t_b, e.cpu_time_total, e.name[:50]))
+        nxt = [e for e in ks if e.time_range.start > t_b]
+        if nxt:
+            print("next device activity at +%.1f us: %s" % (nxt[0].time_range.start - t_b, nxt[0].name[:60]))
