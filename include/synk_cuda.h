@@ -268,6 +268,10 @@ int synk_gemm_prep(synk_dev* dev, int in_dtype, const void* in, uint64_t rows, u
  * output may be NULL. */
 int synk_gemm_prep2_bf16(synk_dev* dev, const float* in, uint64_t rows, uint64_t cols, uint64_t ld_in, void* out,
                          uint64_t ld_out, void* out_t, uint64_t ld_out_t);
+/* The same with an index-fused gather: output row r is input row rowmap[r]
+ * (u64 in HBM); rowmap == NULL is synk_gemm_prep2_bf16. */
+int synk_gemm_prep2_bf16_rows(synk_dev* dev, const float* in, const uint64_t* rowmap, uint64_t rows, uint64_t cols,
+                              uint64_t ld_in, void* out, uint64_t ld_out, void* out_t, uint64_t ld_out_t);
 /* C[M x N] = epilogue(A[M x K] . B[N x K]^T); A, B K-major with leading dims
  * lda/ldb (16-byte aligned rows). C (row-major, ldc) and/or C^T (ldct) may be
  * NULL; out_dtype SYNK_F32 or SYNK_BF16 (act has the same dtype as C). */
@@ -299,14 +303,17 @@ int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, u
 int synk_mlp_loss_grad(synk_dev* dev, int dtype, const uint64_t* dims, uint32_t layers,
                        const void* params, const void* x, const void* y, uint64_t n,
                        double* loss_dev, void* grad, void* workspace, uint64_t workspace_bytes);
+
 /* synk_mlp_loss_grad_ex that, for the bf16 tensor-core path, records
  * synk_signal_slot(dev, signal_base + l) as soon as the gradient segment of
  * layer l ([W_l, b_l] in the flat layout) is final; *signalled = the number
- * of segments signalled (0: nothing signalled, e.g. the native path). */
+ * of segments signalled (0: nothing signalled, e.g. the native path).
+ * rows != NULL (bf16 path): x and y are the whole sources and batch row i is
+ * source row rows[i] -- the bf16 staging of x and the loss read through it. */
 int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
                            void* grad, void* workspace, uint64_t workspace_bytes, int signal_base,
-                           int* signalled);
+                           int* signalled, const uint64_t* rows);
 /* Same with a compute mode: SYNK_MLP_NATIVE runs every product in the
  * parameter dtype on the CUDA cores (f32 FFMA / f64 DFMA); SYNK_MLP_BF16_TC
  * (f32 parameters only) runs every dense product on tcgen05 tensor cores

@@ -87,6 +87,14 @@ struct KernelContext {
     // kernel to signal gradient segments with; it reports them here.
     int grad_signal_base = -1;
     std::vector<GradSegment>* grad_segments = nullptr;
+    // Kernel::fused_index_inputs: for input i, rows != nullptr means input i is
+    // the WHOLE source and row j of the shard is source row rows[j] (u64 in
+    // HBM, count entries, stable for the call); rows == nullptr: gathered.
+    struct IndexedInput {
+        const std::uint64_t* rows = nullptr;
+        std::size_t count = 0;
+    };
+    const std::vector<IndexedInput>* indexed = nullptr;
 };
 
 struct KernelResult {
@@ -116,6 +124,12 @@ struct Kernel {
     KernelFn fn;
     // ---- B200 addition: preferred when set ----
     DeviceKernelFn device_fn;
+    // The device kernel can take a scatter input selected by an index list as
+    // (the whole source in HBM, the selected row numbers) instead of gathered
+    // rows, and gathers inside its own kernels (ctx.indexed): the batch is
+    // never materialised. Used for explicit index lists over an HBM mirror
+    // with num_slices == 1; otherwise inputs arrive gathered as usual.
+    bool fused_index_inputs = false;
 };
 
 struct CallOptions {

@@ -827,24 +827,31 @@ __global__ void __launch_bounds__(256) splitk_fold_kernel(uint32_t S, uint64_t M
 __global__ void __launch_bounds__(256) prep2_bf16_kernel(const float* __restrict__ in, uint64_t rows, uint64_t cols,
                                                          uint64_t ld_in, __nv_bfloat16* __restrict__ out,
                                                          uint64_t ld_out, __nv_bfloat16* __restrict__ out_t,
-                                                         uint64_t ld_out_t, int vec_in) {
+                                                         uint64_t ld_out_t, int vec_in,
+                                                         const uint64_t* __restrict__ rowmap) {
+    // rowmap != nullptr: output row r is input row rowmap[r] (index-fused
+    // gather: the batch is read straight from the whole source).
     __shared__ float tile[64][65];
+    __shared__ uint64_t srow[64];
     const uint64_t r0 = (uint64_t)blockIdx.y * 64, c0 = (uint64_t)blockIdx.x * 64;
     const int t = threadIdx.x;
+    if (t < 64) srow[t] = r0 + t < rows ? (rowmap ? rowmap[r0 + t] : r0 + t) : 0;
+    __syncthreads();
     const int lc = (t % 16) * 4;  // 4 consecutive columns
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
         const int lr = t / 16 + 16 * pass;
         const uint64_t r = r0 + lr, c = c0 + lc;
+        const uint64_t ri = srow[lr];
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (r < rows) {
             if (vec_in && c + 4 <= cols) {
-                const float4 f = __ldcs(reinterpret_cast<const float4*>(in + r * ld_in + c));
+                const float4 f = __ldcs(reinterpret_cast<const float4*>(in + ri * ld_in + c));
                 v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (c + j < cols) v[j] = in[r * ld_in + c + j];
+                    if (c + j < cols) v[j] = in[ri * ld_in + c + j];
             }
         }
 #pragma unroll
@@ -907,9 +914,14 @@ extern "C" {
 
 int synk_gemm_prep2_bf16(synk_dev* d, const float* in, uint64_t rows, uint64_t cols, uint64_t ld_in, void* out,
                          uint64_t ld_out, void* out_t, uint64_t ld_out_t) {
+    return synk_gemm_prep2_bf16_rows(d, in, nullptr, rows, cols, ld_in, out, ld_out, out_t, ld_out_t);
+}
+
+int synk_gemm_prep2_bf16_rows(synk_dev* d, const float* in, const uint64_t* rowmap, uint64_t rows, uint64_t cols,
+                              uint64_t ld_in, void* out, uint64_t ld_out, void* out_t, uint64_t ld_out_t) {
     if (rows == 0 || cols == 0 || (!out && !out_t)) return SYNK_OK;
     synk::DeviceGuard g(d->device);
-    if (!out_t && cols % 8 == 0 && ld_in % 4 == 0 && ld_out % 8 == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
+    if (!rowmap && !out_t && cols % 8 == 0 && ld_in % 4 == 0 && ld_out % 8 == 0 && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) &&
         ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
         // cast only: the vectorised streaming kernel (no shared-memory tile)
         const uint64_t total = rows * (cols / 8);
@@ -922,7 +934,7 @@ int synk_gemm_prep2_bf16(synk_dev* d, const float* in, uint64_t rows, uint64_t c
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
     const int vec_in = (ld_in % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
     prep2_bf16_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out), ld_out,
-                                                   static_cast<__nv_bfloat16*>(out_t), ld_out_t, vec_in);
+                                                   static_cast<__nv_bfloat16*>(out_t), ld_out_t, vec_in, rowmap);
     SYNK_LAUNCHED("prep2_bf16_kernel");
     return SYNK_OK;
 }

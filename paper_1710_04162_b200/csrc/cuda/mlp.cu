@@ -200,13 +200,16 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
                                                               double inv_n, T* __restrict__ delta,
                                                               double* __restrict__ partial,
                                                               unsigned* __restrict__ counter = nullptr,
-                                                              double scale = 0.0, double* __restrict__ loss = nullptr) {
+                                                              double scale = 0.0, double* __restrict__ loss = nullptr,
+                                                              const uint64_t* __restrict__ yrows = nullptr,
+                                                              uint64_t ycols = 1) {
     __shared__ double red[kThreads];
     __shared__ int last;
     double s = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n_el;
          i += (uint64_t)gridDim.x * kThreads) {
-        double diff = __dsub_rn((double)pred[i], (double)y[i]);
+        const uint64_t yi = yrows ? __ldg(yrows + i / ycols) * ycols + i % ycols : i;  // index-fused y
+        double diff = __dsub_rn((double)pred[i], (double)y[yi]);
         s = __dadd_rn(s, __dmul_rn(diff, diff));
         delta[i] = (T)__dmul_rn(diff, inv_n);
     }
@@ -408,7 +411,8 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
 }
 
 int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P, const float* theta, const float* x,
-                   const float* y, uint64_t n, double* loss, float* grad, void* ws, int signal_base = -1) {
+                   const float* y, uint64_t n, double* loss, float* grad, void* ws, int signal_base = -1,
+                   const uint64_t* rows = nullptr) {
     Bf16Plan B = make_bf16_plan(dims, L, n, P.maxd);
     char* base = static_cast<char*>(ws);
     auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
@@ -423,9 +427,9 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
             rc)
             return rc;
     }
-    // input batch: x and x^T in bf16
-    if (int rc = synk_gemm_prep2_bf16(d, x, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]), bf(B.off_actT[0]),
-                                      pad8(n));
+    // input batch: x and x^T in bf16 (rows != null: gathered from the whole source in the same pass)
+    if (int rc = synk_gemm_prep2_bf16_rows(d, x, rows, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]),
+                                           bf(B.off_actT[0]), pad8(n));
         rc)
         return rc;
     {
@@ -458,7 +462,7 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     const double inv_n = 1.0 / (double)n;
     loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial,
                                                                  reinterpret_cast<unsigned*>(d->flags_dev + 3),
-                                                                 0.5 * inv_n, loss);
+                                                                 0.5 * inv_n, loss, rows, dl);
     SYNK_LAUNCHED("loss_delta_kernel");
     int cur = 0;
     if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd),
@@ -629,22 +633,26 @@ int synk_mlp_loss_grad_ex(synk_dev* d, int dtype, int compute, const uint64_t* d
 
 int synk_mlp_loss_grad_seg(synk_dev* d, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev, void* grad,
-                           void* workspace, uint64_t workspace_bytes, int signal_base, int* signalled) {
+                           void* workspace, uint64_t workspace_bytes, int signal_base, int* signalled,
+                           const uint64_t* rows) {
     *signalled = 0;
-    if (compute != SYNK_MLP_BF16_TC || signal_base < 0)
+    if (compute != SYNK_MLP_BF16_TC) {
+        SYNK_REQUIRE(rows == nullptr, SYNK_EARG, "mlp_loss_grad_seg: index-fused rows are a bf16-path feature");
         return synk_mlp_loss_grad_ex(d, dtype, compute, dims, layers, params, x, y, n, loss_dev, grad, workspace,
                                      workspace_bytes);
+    }
     SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
-    SYNK_REQUIRE(signal_base + (int)layers <= 64, SYNK_EARG, "mlp_loss_grad_seg: signal slots out of range");
+    SYNK_REQUIRE(signal_base < 0 || signal_base + (int)layers <= 64, SYNK_EARG,
+                 "mlp_loss_grad_seg: signal slots out of range");
     Plan p;
     if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
     SYNK_REQUIRE(workspace_bytes >= make_bf16_plan(dims, layers, n, p.maxd).total, SYNK_EARG,
                  "mlp: workspace too small");
     synk::DeviceGuard g(d->device);
     const int rc = loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n,
-                                  loss_dev, (float*)grad, workspace, signal_base);
-    if (rc == SYNK_OK) *signalled = (int)layers;
+                                  loss_dev, (float*)grad, workspace, signal_base, rows);
+    if (rc == SYNK_OK && signal_base >= 0) *signalled = (int)layers;
     return rc;
 }
 

@@ -33,6 +33,7 @@ synk_dev* RankDevice::aux_handle() {
 
 RankDevice::~RankDevice() {
     if (aux) synk_close(aux);
+    if (h && index_stage) synk_free(h, index_stage);
     if (staging) synk_host_free(staging);
     if (h && scratch) synk_free(h, scratch);
     if (h) synk_close(h);

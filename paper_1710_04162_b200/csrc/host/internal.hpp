@@ -46,6 +46,12 @@ struct RankDevice {
     // trainer's per-segment all-reduce + update overlapping the backward pass.
     synk_dev* aux = nullptr;
     synk_dev* aux_handle();
+    // Device copy of the rank's part of an index list for index-fused kernel
+    // inputs (grown on demand, reused across calls: a stable address, so the
+    // consuming kernels' CUDA graphs keep hitting). Raw, like `scratch`: a
+    // DevBuffer here would keep its own RankDevice alive.
+    void* index_stage = nullptr;
+    std::size_t index_stage_bytes = 0;
     ~RankDevice();
 };
 

@@ -75,7 +75,8 @@ DevBuffer as_dtype(const std::shared_ptr<detail::RankDevice>& rd, const DevBuffe
 std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::RankDevice>& rd, const Checked& c,
                                                  const DevBuffer& params, const DevBuffer& x, const DevBuffer& y,
                                                  MlpCompute compute = MlpCompute::Native,
-                                                 const KernelContext* ctx = nullptr) {
+                                                 const KernelContext* ctx = nullptr,
+                                                 const std::uint64_t* rows = nullptr) {
     const DType dt = params.dtype();
     if (compute == MlpCompute::Bf16TensorCore && dt != DType::Float32)
         throw DTypeError("mlp_grad_kernel: bf16 tensor-core compute needs float32 parameters");
@@ -92,7 +93,7 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     int signalled = 0;
     detail::check(synk_mlp_loss_grad_seg(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
                                          yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws, ws_bytes,
-                                         base, &signalled),
+                                         base, &signalled, rows),
                   "mlp_loss_grad");
     if (signalled > 0) {
         // Layer l's segment [W_l, b_l] was signalled on slot base + l, in
@@ -180,8 +181,49 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
     k.reads = {block.params};
     const std::vector<FlatSegment> segs = block.segments;
     const std::uint64_t grads_id = block.grads.id();
+    // Index-fused inputs (bf16 path): with x and y selected by the call's index
+    // list over HBM mirrors, the bf16 staging of x reads the batch rows straight
+    // from the whole source and the loss reads y the same way, so the f32 batch
+    // is never gathered. (The native path keeps gathered inputs: an index load
+    // in its latency-bound GEMMs' A loads cost more than the gather it saves.)
+    k.fused_index_inputs = compute == MlpCompute::Bf16TensorCore;
     k.device_fn = [segs, grads_id, compute](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
         const DevBuffer& params = ctx.device_replica(0);
+        const KernelContext::IndexedInput* ix = ctx.indexed ? &(*ctx.indexed)[0] : nullptr;
+        const KernelContext::IndexedInput* iy = ctx.indexed ? &(*ctx.indexed)[1] : nullptr;
+        if (ix && iy && (ix->rows || iy->rows)) {
+            const auto& rd = ctx.rank_device;
+            Checked c = check_operands(params, segs, in[0], in[1]);  // whole sources: same leading extent
+            const bool direct = compute == MlpCompute::Bf16TensorCore && ix->rows && ix->rows == iy->rows &&
+                                ix->count == iy->count && in[0].dtype() == DType::Float32 &&
+                                in[1].dtype() == DType::Float32 && params.dtype() == DType::Float32;
+            if (direct) {
+                c.n = ix->count;
+                auto [loss, grad] = device_loss_grad(rd, c, params, in[0], in[1], compute, &ctx, ix->rows);
+                DeviceKernelResult r;
+                r.outputs.push_back(loss);
+                r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
+                return r;
+            }
+            // Gather the selected rows here, then the regular path.
+            auto gathered = [&](const DevBuffer& src, const KernelContext::IndexedInput& sel) {
+                if (!sel.rows) return src;
+                std::vector<std::size_t> shape = src.shape();
+                shape[0] = sel.count;
+                DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
+                detail::check(synk_gather_rows(rd->h, src.data(), src.rows(), src.row_size() * dtype_size(src.dtype()),
+                                               sel.rows, sel.count, out.data()),
+                              "mlp: gather fused input");
+                return out;
+            };
+            const DevBuffer xg = gathered(in[0], *ix), yg = gathered(in[1], *iy);
+            Checked cg = check_operands(params, segs, xg, yg);
+            auto [loss, grad] = device_loss_grad(rd, cg, params, xg, yg, compute, &ctx);
+            DeviceKernelResult r;
+            r.outputs.push_back(loss);
+            r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
+            return r;
+        }
         Checked c = check_operands(params, segs, in[0], in[1]);
         auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute, &ctx);
         DeviceKernelResult r;

@@ -678,3 +678,36 @@ def test_nccl_backend_optional(sk):
         sk.Trainer(pool, block, sk.SgdRule(), lr=0.1).train_step(f, [x, y])
         g = block.grads.get(0)
         np.testing.assert_allclose(block.params.get(0), p0 - 0.1 * g, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("world,compute", [(1, "bf16"), (2, "bf16"), (3, "bf16"), (2, "native")])
+def test_index_fused_mlp_inputs_bitwise(sk, world, compute):
+    """Index-fused inputs: with x and y HBM-mirrored and selected by an index
+    list, the bf16 MLP kernel stages x straight from the whole source through
+    the row list (gather + bf16 cast + transpose in one pass) and its loss reads
+    y the same way -- no gathered f32 batch. Same arithmetic as the gathered
+    path (un-mirrored inputs): parameters bit for bit after several trainer
+    steps, and the same BoundsError for a bad index."""
+    cfg = sk.MlpConfig(in_dim=256, width=384, out_dim=100, layers=3, seed=1)
+    x, y = sk.mlp_make_dataset(4096, cfg, seed=2, dtype="f32")
+    out = {}
+    for mirror in (True, False):
+        rng = np.random.default_rng(5)
+        with sk.Pool(workers=world) as pool:
+            sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
+            if mirror:
+                sx.mirror(pool)
+                sy.mirror(pool)
+            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+            f = sk.mlp_grad_function(pool, block, compute=compute)
+            sk.distribute(pool)
+            tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.05)
+            losses = [tr.train_step(f, [sx, sy], indexes=rng.integers(0, 4096, 256 * world)) for _ in range(4)]
+            bad = rng.integers(0, 4096, 256 * world)
+            bad[-1] = 4096
+            with pytest.raises(sk.BoundsError):
+                tr.train_step(f, [sx, sy], indexes=bad)
+            assert pool.alive
+            out[mirror] = (losses, block.params.get(world - 1))
+    assert out[True][0] == out[False][0]
+    assert out[True][1].tobytes() == out[False][1].tobytes()
