@@ -451,6 +451,55 @@ def gather_headline(args, n_gpus, devices, dist, world):
     # latency of a single 4096-row batch (the per-call granularity of the config)
     _, single_s = gather_launches(B, 50, 5)
 
+    # ---- the same gather with the dataset left in pinned, mapped HOST memory
+    # (the paper's default: rows pulled over PCIe by the kernel), against the
+    # PCIe copy bandwidth measured here (1 GiB pinned source, 256 MiB per launch)
+    host_src = None
+    if not dist or dist.get_rank() == 0:
+        h = handles[0]
+        hbytes = 1 << 30
+        hp = vp()
+        ok(lib.synk_host_alloc(u64(hbytes), ctypes.byref(hp)), "host alloc")
+        try:
+            ctypes.memset(hp, 0x3F, hbytes)
+            hrows = hbytes // row_bytes
+            hidx = rng.integers(0, hrows, n_step).astype(np.uint64)
+            d_hidx, d_out, d_cpy = vp(), vp(), vp()
+            ok(lib.synk_alloc(h, u64(hidx.nbytes), ctypes.byref(d_hidx)), "alloc")
+            ok(lib.synk_alloc(h, u64(n_step * row_bytes), ctypes.byref(d_out)), "alloc")
+            ok(lib.synk_alloc(h, u64(n_step * row_bytes), ctypes.byref(d_cpy)), "alloc")
+            ok(lib.synk_copy(h, d_hidx, hidx.ctypes.data_as(vp), u64(hidx.nbytes)), "H2D idx")
+            ok(lib.synk_sync(h), "sync")
+
+            def timed(fn, reps=5):
+                for _ in range(2):
+                    fn()
+                m0, m1 = ctypes.c_int(), ctypes.c_int()
+                ok(lib.synk_mark_reset(h), "marks")
+                ok(lib.synk_mark(h, ctypes.byref(m0)), "mark")
+                for _ in range(reps):
+                    fn()
+                ok(lib.synk_mark(h, ctypes.byref(m1)), "mark")
+                ok(lib.synk_sync(h), "sync")
+                sec = ctypes.c_double()
+                ok(lib.synk_mark_elapsed(h, m0.value, m1.value, ctypes.byref(sec)), "elapsed")
+                return sec.value / reps
+
+            t_g = timed(lambda: ok(lib.synk_gather_rows(h, hp, u64(hrows), u64(row_bytes), d_hidx, u64(n_step),
+                                                        d_out), "gather (host source)"))
+            t_c = timed(lambda: ok(lib.synk_copy(h, d_cpy, hp, u64(n_step * row_bytes)), "H2D copy"))
+            pcie = n_step * row_bytes / t_c / 1e9
+            over_pcie = n_step * row_bytes / t_g / 1e9
+            host_src = {"config": "C2 gather with the dataset in pinned, mapped host memory (1 GiB sample, %d rows "
+                                  "per launch): rows travel over PCIe inside the gather kernel" % n_step,
+                        "row_gbs_over_pcie": over_pcie, "pcie_h2d_copy_gbs": pcie,
+                        "frac_of_pcie_copy": over_pcie / pcie, "us_per_launch": 1e6 * t_g}
+            for p_ in (d_hidx, d_out, d_cpy):
+                lib.synk_free(h, p_)
+            ok(lib.synk_sync(h), "sync")
+        finally:
+            lib.synk_host_free(hp)
+
     # ---- e2e through the public API --------------------------------------------------
     f = sk.make_function(pool, sk.row_count_kernel(), ["scatter"], ["sum"])
     sk.distribute(pool)
@@ -484,7 +533,7 @@ def gather_headline(args, n_gpus, devices, dist, world):
     pool.shutdown()
     del arr
     return {"value": value, "region_s": region_s, "e2e": e2e, "e2e_breakdown": e2e_breakdown, "achieved": achieved,
-            "single_s": single_s, "clocks": clocks.summary(),
+            "single_s": single_s, "clocks": clocks.summary(), "host_source": host_src,
             "setup_s": setup_s, "n_step": n_step, "row_bytes": row_bytes, "peak": peak, "peak_kind": peak_kind}
 
 
@@ -649,6 +698,7 @@ def ours(args, n_gpus, dist=None, world=1, local_device=0):
                          "traffic_unit": "bytes/launch", "peak_kind": peak_kind,
                          "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
             "single_batch_us": 1e6 * hd["single_s"],
+            "gather_from_host_memory": hd["host_source"],
             "gpu_launches": n_gpus * args.steps, "clocks": hd["clocks"], "setup_s": hd["setup_s"]}
     if dist is not None:
         line["processes"] = "one per GPU for the headline (torchrun); rank 0 alone for the sub-measurements"
