@@ -187,6 +187,22 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
     // is never gathered. (The native path keeps gathered inputs: an index load
     // in its latency-bound GEMMs' A loads cost more than the gather it saves.)
     k.fused_index_inputs = compute == MlpCompute::Bf16TensorCore;
+    // The reference's host-kernel contract as well (mlp.cpp:249-265): user code
+    // may wrap `kernel.fn` (e.g. to re-emit the gradient as an Add update).
+    // It computes on the calling rank's GPU from host buffers.
+    k.fn = [segs, grads_id, compute](const std::vector<NdBuffer>& in, const KernelContext& ctx) {
+        auto rd = ctx.rank_device ? ctx.rank_device : detail::utility_device();
+        const NdBuffer& params_h = ctx.replica(0);
+        Checked c = check_operands(params_h, segs, in[0], in[1]);
+        DevBuffer p = detail::dev_from_host(rd, params_h);
+        DevBuffer xd = detail::dev_from_host(rd, in[0]);
+        DevBuffer yd = detail::dev_from_host(rd, in[1]);
+        auto [loss, grad] = device_loss_grad(rd, c, p, xd, yd, compute);
+        KernelResult r;
+        r.outputs.push_back(NdBuffer::scalar(detail::dev_to_host(loss).get(0)));
+        r.updates.push_back(UpdateDelta{grads_id, detail::dev_to_host(grad), UpdateCombine::WeightedMeanByRows});
+        return r;
+    };
     k.device_fn = [segs, grads_id, compute](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
         const DevBuffer& params = ctx.device_replica(0);
         const KernelContext::IndexedInput* ix = ctx.indexed ? &(*ctx.indexed)[0] : nullptr;

@@ -711,3 +711,22 @@ def test_index_fused_mlp_inputs_bitwise(sk, world, compute):
             out[mirror] = (losses, block.params.get(world - 1))
     assert out[True][0] == out[False][0]
     assert out[True][1].tobytes() == out[False][1].tobytes()
+
+
+def test_reference_acceptance_battery_on_our_executor():
+    """The reference's own acceptance battery (tests/acceptance_main.cpp),
+    compiled UNCHANGED against our headers and linked with our library
+    (oracle/Makefile target acceptance_ours, built where the reference sources
+    are): every criterion passes or is skipped (criterion 6 measures CPU
+    thread scaling and skips when its W=4 ranks share one GPU)."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "acceptance_ours")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/acceptance_ours not built (needs the reference sources)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert "[FAIL]" not in out.stdout, out.stdout
