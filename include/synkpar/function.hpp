@@ -217,6 +217,10 @@ ParallelFunction function(WorkerPool& pool, Kernel kernel, std::vector<InputSpec
 void distribute(WorkerPool& pool);
 
 // ---- B200 built-in device kernels (the payloads of the benchmark configs) ----
+// In their own namespace, so the reference namespace gains no names a user
+// program (e.g. the reference's own tests, which define an identity_kernel())
+// could collide with.
+namespace device_kernels {
 // "identity": output 0 = the shard itself (Gather it for zero-copy concat).
 Kernel identity_kernel(std::string name = "identity");
 // "row_count": output 0 = f64 scalar rows of the shard (a no-op payload that
@@ -226,5 +230,6 @@ Kernel row_count_kernel(std::string name = "row_count");
 // (Sum, Max, Gather) -- the slicing/aggregation config of the benchmark.
 // with_shard=false drops the third output (declare only Sum, Max).
 Kernel column_stats_kernel(std::string name = "column_stats", bool with_shard = true);
+} // namespace device_kernels
 
 } // namespace synkpar

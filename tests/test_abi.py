@@ -151,3 +151,27 @@ def test_synk_streamed_io_and_shared_input_from_file(sk, tmp_path, dtype):
     with open(path, "wb") as fh:
         fh.write(blob + b"trailing")  # the reference ignores bytes past the payload
     np.testing.assert_array_equal(sk.load_tensor(path), data)
+
+
+def test_doctest_shim_detects_failures(tmp_path):
+    """The doctest-compatible shim used to compile the reference's unit tests
+    against this repository really fails on failing checks (CPU only)."""
+    import subprocess
+
+    from conftest import ROOT
+
+    src = tmp_path / "t.cpp"
+    src.write_text("\n".join([
+        "#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN",
+        "#include <doctest.h>",
+        "#include <stdexcept>",
+        'TEST_CASE("ok") { CHECK(1 + 1 == 2); CHECK_THROWS_AS(throw std::runtime_error("x"), std::runtime_error);'
+        " CHECK(0.1 + 0.2 == doctest::Approx(0.3)); }",
+        'TEST_CASE("bad") { CHECK(1 + 1 == 3); REQUIRE(false); }',
+        ""]))
+    exe = tmp_path / "t"
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-I", os.path.join(ROOT, "tests", "doctest_shim"), str(src), "-o",
+                    str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 1
+    assert "2 passed" not in out.stdout and "1 passed | 1 failed" in out.stdout

@@ -730,3 +730,21 @@ def test_reference_acceptance_battery_on_our_executor():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert "[FAIL]" not in out.stdout, out.stdout
+
+
+def test_reference_unit_tests_on_our_executor():
+    """The reference's C++ unit tests (117 test cases: tensor, tensor_io,
+    worker_pool, shared_input, replicated, function, sgd, mlp, bench), compiled
+    UNCHANGED against our headers and library with our doctest-compatible shim
+    (oracle/Makefile target unit_ours): all pass on the B200 executor."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "unit_ours")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/unit_ours not built (needs the reference sources)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    assert "0 failed" in out.stdout
