@@ -748,3 +748,24 @@ def test_reference_unit_tests_on_our_executor():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
     assert "0 failed" in out.stdout
+
+
+def test_reference_python_binding_on_our_executor():
+    """The reference's own pybind11 module (bindings/pymodule.cpp), compiled
+    unchanged against our headers and linked with our library
+    (oracle/_ref/ours_binding): its Python API driven end to end on the B200
+    executor (separate interpreter: two pybind11 modules binding the same C++
+    types cannot share one)."""
+    import glob
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    if not glob.glob(os.path.join(ROOT, "oracle", "_ref", "ours_binding", "_synkpar*.so")):
+        pytest.skip("oracle/_ref/ours_binding not built (needs the reference sources)")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "ref_binding_checks.py")], capture_output=True,
+                         text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "ok" in out.stdout
