@@ -1018,8 +1018,18 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
     uint32_t splits = 1;
     if (tiles < 148 && num_kb >= 16 && (epilogue == SYNK_EPI_STORE || epilogue == SYNK_EPI_BIAS) &&
         out_dtype == SYNK_F32 && !ct && c) {
-        uint64_t sp = 296 / tiles;  // one wave of 2 CTAs per SM
-        sp = std::min<uint64_t>(sp, num_kb / 8);
+        // one wave of 2 CTAs per SM, >= 8 K blocks per split (SYNK_SPLITK_CTAS /
+        // SYNK_SPLITK_MINKB override: diagnostics)
+        static const uint64_t target = [] {
+            const char* v = getenv("SYNK_SPLITK_CTAS");
+            return v ? (uint64_t)atoll(v) : (uint64_t)296;
+        }();
+        static const uint64_t min_kb = [] {
+            const char* v = getenv("SYNK_SPLITK_MINKB");
+            return v ? (uint64_t)atoll(v) : (uint64_t)8;
+        }();
+        uint64_t sp = target / tiles;
+        sp = std::min<uint64_t>(sp, num_kb / min_kb);
         splits = (uint32_t)std::max<uint64_t>(sp, 1);
     }
     if (splits > 1) {
