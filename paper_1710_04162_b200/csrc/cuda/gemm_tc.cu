@@ -201,11 +201,76 @@ struct ActPrefetch {
     }
 };
 
+// Split-K fold through distributed shared memory (cluster = the S split CTAs
+// of one output tile, cluster rank = blockIdx.z): every CTA parks its fp32
+// partial tile in its own (now idle) operand ring, the cluster syncs, CTA z
+// folds rows [z*R, (z+1)*R) across the S partials in rank order with an f64
+// accumulator (the same order and rounding as splitk_fold_kernel), adds the
+// bias and writes C; a second cluster sync keeps every partial alive until
+// its readers are done. Replaces S fp32 planes in HBM and the fold launch.
+constexpr int kFoldPitch = BN + 4;  // floats; +4 spreads the row-per-lane stores over the banks
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NT>
+__device__ __forceinline__ void cluster_fold_epilogue(const EpiArgs& epi, float* part, uint32_t lane_base, int row,
+                                                      int c_begin, int c_count, uint32_t m0, uint32_t n0, uint32_t M,
+                                                      uint32_t N) {
+#pragma unroll 1
+    for (int c0 = c_begin; c0 < c_begin + c_count; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(lane_base + c0, r);
+        float4* dst = reinterpret_cast<float4*>(part + row * kFoldPitch + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                                 __uint_as_float(r[4 * j + 3]));
+    }
+    cluster_sync_all();
+    uint32_t me, S;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(me));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(S));
+    const uint32_t rows_per = (BM + S - 1) / S, r_begin = me * rows_per;
+    const uint32_t r_end = min((uint32_t)BM, r_begin + rows_per);
+    const uint32_t local = (uint32_t)__cvta_generic_to_shared(part);
+    float* C = static_cast<float*>(epi.c);
+    constexpr int kQuads = BN / 4;  // float4 columns per row
+    for (uint32_t i = threadIdx.x; i < (r_end - r_begin) * kQuads; i += NT) {
+        const uint32_t rr = r_begin + i / kQuads, cc = (i % kQuads) * 4;
+        const uint32_t off = local + (rr * kFoldPitch + cc) * 4;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (uint32_t s = 0; s < S; ++s) {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(off), "r"(s));
+            float x0, x1, x2, x3;
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+                         : "r"(remote)
+                         : "memory");
+            a0 += (double)x0, a1 += (double)x1, a2 += (double)x2, a3 += (double)x3;
+        }
+        const uint64_t m = (uint64_t)m0 + rr;
+        if (m >= M) continue;
+        const double a[4] = {a0, a1, a2, a3};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t n = (uint64_t)n0 + cc + j;
+            if (n >= N) break;
+            float v = (float)a[j];
+            if (epi.mode == EPI_BIAS) v += epi.bias[n];
+            C[m * epi.ldc + n] = v;
+        }
+    }
+    cluster_sync_all();
+}
+
 template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
 __global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
-                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per, uint32_t layout) {
+                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per, uint32_t layout, int cfold) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -222,7 +287,7 @@ __global__ void __launch_bounds__(NT, 2)
     const int kb0 = (int)(blockIdx.z * kb_per);
     const int num_kb = min((int)kb_per, (int)((K + kBK - 1) / kBK) - kb0);
     const int total = passes * num_kb;
-    if (gridDim.z > 1) epi.c = static_cast<float*>(epi.c) + (uint64_t)blockIdx.z * M * epi.ldc;
+    if (gridDim.z > 1 && !cfold) epi.c = static_cast<float*>(epi.c) + (uint64_t)blockIdx.z * M * epi.ldc;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -305,6 +370,14 @@ __global__ void __launch_bounds__(NT, 2)
     // Row-major C: 16 consecutive columns per thread -> 16-byte vector stores
     // when the row pitch allows; C^T: lanes hold consecutive rows -> each
     // scalar store instruction is one coalesced warp-wide segment.
+    if (cfold) {
+        cluster_fold_epilogue<NT>(epi, reinterpret_cast<float*>(smem), lane_base, quad * 32 + lane, grp * kCols,
+                                  kCols, m0, n0, M, N);
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+        return;
+    }
     const int es = epi.out_bf16 ? 2 : 4;
     const bool vec_c = epi.c && ((epi.ldc * es) % 16 == 0) && ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
     const bool vec_act = epi.mode == EPI_TANH_GRAD && ((epi.ldact * es) % 16 == 0) &&
@@ -734,7 +807,7 @@ constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
-           uint32_t kb_per = 0x7fffffffu, uint32_t layout = 0) {
+           uint32_t kb_per = 0x7fffffffu, uint32_t layout = 0, int cfold = 0) {
     // Epilogue-heavy launches (short K, or the tanh-derivative reading the
     // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
     // the full register budget. SYNK_GEMM_WARPS=4|8 overrides (A/B runs).
@@ -744,16 +817,35 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
     }();
     const bool wide = forced ? forced == 8 : (K <= 512 || e.mode == EPI_TANH_GRAD);
     dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), splits);
+    if (cfold) {  // the split CTAs of a tile form one cluster (DSMEM fold)
+        auto kern = wide ? gemm_tc_kernel<KIND, 256> : gemm_tc_kernel<KIND, 128>;
+        if (int rc = synk::ensure_max_smem((const void*)kern, d->device, (int)kSmemBytes); rc) return rc;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(wide ? 256 : 128);
+        cfg.dynamicSmemBytes = kSmemBytes;
+        cfg.stream = d->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = splits;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SYNK_CU(cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N, (uint32_t)K, e, kb_per,
+                                   layout, 1));
+        return SYNK_OK;
+    }
     if (wide) {
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 256>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per, layout);
+                                                                       (uint32_t)K, e, kb_per, layout, 0);
     } else {
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 128>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per, layout);
+                                                                       (uint32_t)K, e, kb_per, layout, 0);
     }
     SYNK_LAUNCHED("gemm_tc_kernel");
     return SYNK_OK;
@@ -1035,6 +1127,18 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
     if (splits > 1) {
         const uint32_t kb_per = (uint32_t)((num_kb + splits - 1) / splits);
         splits = (uint32_t)((num_kb + kb_per - 1) / kb_per);
+        // Up to 8 splits (a portable cluster): fold through distributed shared
+        // memory inside the GEMM (same order and rounding as the fold kernel).
+        // SYNK_SPLITK_CLUSTER=0 keeps the fp32 planes + fold kernel (A/B runs).
+        static const bool cluster_fold = [] {
+            const char* v = getenv("SYNK_SPLITK_CLUSTER");
+            return !(v && v[0] == '0');
+        }();
+        if (cluster_fold && bf16 && splits <= 8) {
+            EpiArgs ce{epilogue == SYNK_EPI_BIAS ? EPI_BIAS : EPI_STORE, 0, c, ldc, nullptr, 0,
+                       epilogue == SYNK_EPI_BIAS ? bias : nullptr, nullptr, 0};
+            return launch<0>(d, 1, a0, a1, b0, b1, M, N, K, ce, splits, kb_per, lay, 1);
+        }
         float* planes = nullptr;
         SYNK_CU(cudaMallocAsync((void**)&planes, (size_t)splits * M * N * sizeof(float), d->stream));
         EpiArgs pe{SYNK_EPI_STORE, 0, planes, N, nullptr, 0, nullptr, nullptr, 0};

@@ -174,6 +174,42 @@ def test_bf16_split_k_small_n(M, N, K, epi):
     assert got.tobytes() == again.tobytes()
 
 
+def _split_case(M, N, K, epi):
+    rng = np.random.default_rng(M * 3 + N + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)))
+    bias = rng.uniform(-1, 1, N).astype(np.float32)
+    with Ranks(1) as R:
+        got, _ = gemm(R, "bf16", a, b, epi, bias if epi == "bias" else None)
+    return a, b, bias, got
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(8192, 100, 4096, "bias"), (4097, 100, 8192, "store"), (1000, 100, 1536, "bias"),
+                                       (200, 10, 4096, "bias"), (300, 64, 2000, "store")])
+def test_split_k_cluster_fold_matches_planes(M, N, K, epi, tmp_path):
+    """Split-K with <= 8 splits folds its partials through distributed shared
+    memory inside a cluster (2, 3, 4 and 8 splits here; ragged M, N and fold
+    rows). It must equal the fp32-planes + fold-kernel path bit for bit (same
+    order, f64 accumulator), which runs in a subprocess with
+    SYNK_SPLITK_CLUSTER=0, and meet the unsplit accuracy bar."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    a, b, bias, got = _split_case(M, N, K, epi)
+    want = a.astype(np.float64) @ b.astype(np.float64).T + (bias if epi == "bias" else 0)
+    assert rel_err(got, want) <= 1e-6 + 5e-8 * K
+    out = tmp_path / "planes.npy"
+    code = ("import sys, numpy as np; sys.path.insert(0, 'tests'); from test_gpu_gemm import _split_case; "
+            f"np.save({str(out)!r}, _split_case({M}, {N}, {K}, {epi!r})[3])")
+    env = dict(os.environ, SYNK_SPLITK_CLUSTER="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert np.load(out).tobytes() == got.tobytes()
+
+
 @pytest.mark.parametrize("rows,cols", [(64, 64), (1000, 100), (37, 5), (130, 2048)])
 def test_prep2_bf16_cast_and_transpose(rows, cols):
     rng = np.random.default_rng(rows * cols)
