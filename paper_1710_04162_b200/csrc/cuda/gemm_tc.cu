@@ -1137,7 +1137,11 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         if (cluster_fold && bf16 && splits <= 8) {
             EpiArgs ce{epilogue == SYNK_EPI_BIAS ? EPI_BIAS : EPI_STORE, 0, c, ldc, nullptr, 0,
                        epilogue == SYNK_EPI_BIAS ? bias : nullptr, nullptr, 0};
-            return launch<0>(d, 1, a0, a1, b0, b1, M, N, K, ce, splits, kb_per, lay, 1);
+            const int rc = launch<0>(d, 1, a0, a1, b0, b1, M, N, K, ce, splits, kb_per, lay, 1);
+            if (rc == SYNK_OK) return rc;
+            // a cluster of `splits` CTAs that cannot be scheduled here (e.g. an
+            // SM-limited context): clear the launch error, take the planes path
+            cudaGetLastError();
         }
         float* planes = nullptr;
         SYNK_CU(cudaMallocAsync((void**)&planes, (size_t)splits * M * N * sizeof(float), d->stream));
