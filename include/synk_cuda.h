@@ -308,8 +308,10 @@ int synk_mlp_loss_grad(synk_dev* dev, int dtype, const uint64_t* dims, uint32_t 
  * synk_signal_slot(dev, signal_base + l) as soon as the gradient segment of
  * layer l ([W_l, b_l] in the flat layout) is final; *signalled = the number
  * of segments signalled (0: nothing signalled, e.g. the native path).
- * rows != NULL (bf16 path): x and y are the whole sources and batch row i is
- * source row rows[i] -- the bf16 staging of x and the loss read through it. */
+ * rows != NULL: x and y are the whole sources and batch row i is source row
+ * rows[i] (u64 in device memory, n entries, every entry a valid row: the
+ * caller checks the list) -- the bf16 staging of x (bf16 path) or a gather
+ * inside the launch sequence (native path) and the loss read through it. */
 int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
                            void* grad, void* workspace, uint64_t workspace_bytes, int signal_base,

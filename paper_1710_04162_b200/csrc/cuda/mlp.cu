@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
 
 struct Plan {
     uint64_t woff[64], boff[64];
-    uint64_t total = 0, maxd = 0, act_elems = 0, splitk = 0;
+    uint64_t total = 0, maxd = 0, act_elems = 0, splitk = 0, in_dim = 0;
 };
 
 int make_plan(const uint64_t* dims, uint32_t layers, uint64_t n, Plan* p) {
@@ -261,27 +261,43 @@ int make_plan(const uint64_t* dims, uint32_t layers, uint64_t n, Plan* p) {
     }
     for (uint32_t l = 0; l <= layers; ++l) p->maxd = dims[l] > p->maxd ? dims[l] : p->maxd;
     p->total = at;
+    p->in_dim = dims[0];
     p->splitk = splitk_elems(4, dims, layers, n);  // f32 only; f64 products are not split
     return SYNK_OK;
 }
 
 constexpr int kLossBlocks = 592;  // 4 CTAs per SM of a B200
 
-// workspace: acts[1..L] | delta ping | delta pong | loss partials | split-K partials
-uint64_t ws_bytes(int dtype, const Plan& p, uint64_t n) {
-    uint64_t es = synk::dtype_bytes(dtype);
+// workspace: acts[1..L] | delta ping | delta pong | loss partials | split-K partials | gathered x
+uint64_t xg_offset(uint64_t es, const Plan& p, uint64_t n) {
     uint64_t bytes = (p.act_elems + 2 * n * p.maxd) * es;
     bytes = (bytes + 255) / 256 * 256;
-    return bytes + kLossBlocks * sizeof(double) + (es == 4 ? p.splitk * es : 0);
+    bytes += kLossBlocks * sizeof(double) + (es == 4 ? p.splitk * es : 0);
+    return (bytes + 255) / 256 * 256;
+}
+
+uint64_t ws_bytes(int dtype, const Plan& p, uint64_t n) {
+    const uint64_t es = synk::dtype_bytes(dtype);
+    return xg_offset(es, p, n) + n * p.in_dim * es;
 }
 
 template <class T>
 int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& P, const T* theta,
-                const T* x, const T* y, uint64_t n, double* loss, T* grad, void* ws) {
-    // workspace: acts[1..L] | delta ping | delta pong | loss partials
+                const T* x, const T* y, uint64_t n, double* loss, T* grad, void* ws,
+                const uint64_t* rows = nullptr) {
+    // workspace: acts[1..L] | delta ping | delta pong | loss partials | split-K | gathered x
     T* base = (T*)ws;
     T* acts[65];
     acts[0] = const_cast<T*>(x);
+    if (rows) {
+        // Index-fused inputs: x and y are the whole sources and row i of the
+        // batch is source row rows[i] (valid: the caller checked the list).
+        // x is gathered into the workspace by the first launch of the sequence
+        // (inside the CUDA graph), y is read through the list by the loss kernel.
+        T* xg = (T*)((char*)ws + xg_offset(sizeof(T), P, n));
+        if (int rc = synk_gather_rows(d, x, ~0ull, dims[0] * sizeof(T), rows, n, xg); rc) return rc;
+        acts[0] = xg;
+    }
     T* cur = base;
     for (uint32_t l = 1; l <= layers; ++l) {
         acts[l] = cur;
@@ -310,7 +326,7 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     double inv_n = 1.0 / (double)n;
     loss_delta_kernel<T><<<blocks, kThreads, 0, d->stream>>>(acts[layers], y, n_el, inv_n, dA, partial,
                                                              reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n,
-                                                             loss);
+                                                             loss, rows, dims[layers]);
     SYNK_LAUNCHED("loss_delta_kernel");
 
     T* delta = dA;
@@ -515,12 +531,12 @@ struct GraphKey {
     uint32_t layers;
     uint64_t dims[65];
     uint64_t n;
-    const void* ptrs[6];
+    const void* ptrs[7];
     bool operator==(const GraphKey& o) const {
         if (dtype != o.dtype || layers != o.layers || n != o.n) return false;
         for (uint32_t l = 0; l <= layers && l < 65; ++l)
             if (dims[l] != o.dims[l]) return false;
-        for (int i = 0; i < 6; ++i)
+        for (int i = 0; i < 7; ++i)
             if (ptrs[i] != o.ptrs[i]) return false;
         return true;
     }
@@ -599,6 +615,12 @@ void release_graphs(synk_dev* d) {
 
 namespace {
 
+// Native (FFMA/DFMA) loss/grad, the whole launch sequence replayed from a CUDA
+// graph; rows != null: index-fused x/y (see loss_grad_t).
+int native_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t layers, const void* params, const void* x,
+                     const void* y, uint64_t n, double* loss_dev, void* grad, void* workspace,
+                     uint64_t workspace_bytes, const uint64_t* rows);
+
 }  // namespace
 
 extern "C" {
@@ -637,9 +659,9 @@ int synk_mlp_loss_grad_seg(synk_dev* d, int dtype, int compute, const uint64_t* 
                            const uint64_t* rows) {
     *signalled = 0;
     if (compute != SYNK_MLP_BF16_TC) {
-        SYNK_REQUIRE(rows == nullptr, SYNK_EARG, "mlp_loss_grad_seg: index-fused rows are a bf16-path feature");
-        return synk_mlp_loss_grad_ex(d, dtype, compute, dims, layers, params, x, y, n, loss_dev, grad, workspace,
-                                     workspace_bytes);
+        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE, SYNK_EARG, "mlp: unknown compute mode");
+        return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
+                                rows);
     }
     SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
@@ -668,6 +690,17 @@ int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, u
 int synk_mlp_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t layers,
                        const void* params, const void* x, const void* y, uint64_t n,
                        double* loss_dev, void* grad, void* workspace, uint64_t workspace_bytes) {
+    return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
+                            nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+
+int native_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t layers, const void* params, const void* x,
+                     const void* y, uint64_t n, double* loss_dev, void* grad, void* workspace,
+                     uint64_t workspace_bytes, const uint64_t* rows) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "mlp: bad dtype");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
     Plan p;
@@ -677,9 +710,9 @@ int synk_mlp_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t la
     auto launch_all = [&]() {
         if (dtype == SYNK_F32)
             return loss_grad_t<float>(d, dims, layers, p, (const float*)params, (const float*)x,
-                                      (const float*)y, n, loss_dev, (float*)grad, workspace);
+                                      (const float*)y, n, loss_dev, (float*)grad, workspace, rows);
         return loss_grad_t<double>(d, dims, layers, p, (const double*)params, (const double*)x,
-                                   (const double*)y, n, loss_dev, (double*)grad, workspace);
+                                   (const double*)y, n, loss_dev, (double*)grad, workspace, rows);
     };
     GraphKey key{};
     key.dtype = dtype;
@@ -687,8 +720,8 @@ int synk_mlp_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t la
     for (uint32_t l = 0; l <= layers && l < 65; ++l) key.dims[l] = dims[l];
     key.n = n;
     key.ptrs[0] = params, key.ptrs[1] = x, key.ptrs[2] = y, key.ptrs[3] = loss_dev, key.ptrs[4] = grad;
-    key.ptrs[5] = workspace;
+    key.ptrs[5] = workspace, key.ptrs[6] = rows;
     return graph_launch(d, key, launch_all);
 }
 
-}  // extern "C"
+}  // namespace

@@ -181,12 +181,13 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
     k.reads = {block.params};
     const std::vector<FlatSegment> segs = block.segments;
     const std::uint64_t grads_id = block.grads.id();
-    // Index-fused inputs (bf16 path): with x and y selected by the call's index
-    // list over HBM mirrors, the bf16 staging of x reads the batch rows straight
-    // from the whole source and the loss reads y the same way, so the f32 batch
-    // is never gathered. (The native path keeps gathered inputs: an index load
-    // in its latency-bound GEMMs' A loads cost more than the gather it saves.)
-    k.fused_index_inputs = compute == MlpCompute::Bf16TensorCore;
+    // Index-fused inputs: with x and y selected by the call's index list over
+    // HBM mirrors, the loss reads y through the list and x is staged from the
+    // whole source inside the kernel's own launch sequence -- the bf16 staging
+    // of x reads the batch rows straight from the source (the f32 batch is
+    // never gathered); the native path gathers x as the first node of its CUDA
+    // graph (one graph launch per step instead of two gathers + the graph).
+    k.fused_index_inputs = true;
     // The reference's host-kernel contract as well (mlp.cpp:249-265): user code
     // may wrap `kernel.fn` (e.g. to re-emit the gradient as an Add update).
     // It computes on the calling rank's GPU from host buffers.
@@ -210,9 +211,9 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
         if (ix && iy && (ix->rows || iy->rows)) {
             const auto& rd = ctx.rank_device;
             Checked c = check_operands(params, segs, in[0], in[1]);  // whole sources: same leading extent
-            const bool direct = compute == MlpCompute::Bf16TensorCore && ix->rows && ix->rows == iy->rows &&
-                                ix->count == iy->count && in[0].dtype() == DType::Float32 &&
-                                in[1].dtype() == DType::Float32 && params.dtype() == DType::Float32;
+            const bool direct = ix->rows && ix->rows == iy->rows && ix->count == iy->count &&
+                                in[0].dtype() == params.dtype() && in[1].dtype() == params.dtype() &&
+                                (compute == MlpCompute::Native || params.dtype() == DType::Float32);
             if (direct) {
                 c.n = ix->count;
                 auto [loss, grad] = device_loss_grad(rd, c, params, in[0], in[1], compute, &ctx, ix->rows);

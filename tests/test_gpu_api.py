@@ -680,16 +680,18 @@ def test_nccl_backend_optional(sk):
         np.testing.assert_allclose(block.params.get(0), p0 - 0.1 * g, rtol=0, atol=1e-15)
 
 
-@pytest.mark.parametrize("world,compute", [(1, "bf16"), (2, "bf16"), (3, "bf16"), (2, "native")])
-def test_index_fused_mlp_inputs_bitwise(sk, world, compute):
+@pytest.mark.parametrize("world,compute,dtype", [(1, "bf16", "f32"), (2, "bf16", "f32"), (3, "bf16", "f32"),
+                                                 (1, "native", "f32"), (2, "native", "f32"), (2, "native", "f64")])
+def test_index_fused_mlp_inputs_bitwise(sk, world, compute, dtype):
     """Index-fused inputs: with x and y HBM-mirrored and selected by an index
-    list, the bf16 MLP kernel stages x straight from the whole source through
-    the row list (gather + bf16 cast + transpose in one pass) and its loss reads
-    y the same way -- no gathered f32 batch. Same arithmetic as the gathered
-    path (un-mirrored inputs): parameters bit for bit after several trainer
-    steps, and the same BoundsError for a bad index."""
+    list, the MLP kernel reads the batch rows from the whole sources itself --
+    the bf16 path stages x through the row list (gather + bf16 cast + transpose
+    in one pass), the native path gathers x as the first node of its CUDA
+    graph, and both losses read y through the list. Same arithmetic as the
+    gathered path (un-mirrored inputs): parameters bit for bit after several
+    trainer steps, and the same BoundsError for a bad index."""
     cfg = sk.MlpConfig(in_dim=256, width=384, out_dim=100, layers=3, seed=1)
-    x, y = sk.mlp_make_dataset(4096, cfg, seed=2, dtype="f32")
+    x, y = sk.mlp_make_dataset(4096, cfg, seed=2, dtype=dtype)
     out = {}
     for mirror in (True, False):
         rng = np.random.default_rng(5)
@@ -698,7 +700,7 @@ def test_index_fused_mlp_inputs_bitwise(sk, world, compute):
             if mirror:
                 sx.mirror(pool)
                 sy.mirror(pool)
-            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, dtype))
             f = sk.mlp_grad_function(pool, block, compute=compute)
             sk.distribute(pool)
             tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.05)
