@@ -54,6 +54,38 @@ struct Vec<1> {
     using T = uint8_t;
     static __device__ __forceinline__ T load(const T* p) { return __ldg(p); }
 };
+// 256-bit vectors (sm_100 ld/st .v8.b32): one instruction per 32 bytes per lane
+struct alignas(32) U8x32 {
+    uint32_t w[8];
+};
+template <>
+struct Vec<32> {
+    using T = U8x32;
+    static __device__ __forceinline__ T load(const T* p) {
+        T r;
+        asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                       "=r"(r.w[6]), "=r"(r.w[7])
+                     : "l"(p));
+        return r;
+    }
+};
+
+template <class T>
+__device__ __forceinline__ void store_vec(T* p, const T& v, int streaming) {
+    if (streaming) __stcs(p, v);
+    else *p = v;
+}
+__device__ __forceinline__ void store_vec(U8x32* p, const U8x32& v, int streaming) {
+    if (streaming)
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                     "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                     : "memory");
+    else
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                     "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                     : "memory");
+}
 
 constexpr int kBlock = 256;
 
@@ -113,10 +145,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
 #pragma unroll
                     for (int u = 0; u < kUnroll; ++u) {
                         uint64_t v = v0 + (uint64_t)u * 32;
-                        if (exists[k] && v < row_vecs) {
-                            if (stream_stores) __stcs(dst + (r0 + k) * row_vecs + v, buf[k][u]);
-                            else dst[(r0 + k) * row_vecs + v] = buf[k][u];
-                        }
+                        if (exists[k] && v < row_vecs) store_vec(dst + (r0 + k) * row_vecs + v, buf[k][u], stream_stores);
                     }
             }
         }
@@ -153,7 +182,10 @@ int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
     uint64_t blocks = (chunks * 32 + kBlock - 1) / kBlock;
     const uint64_t cap = (uint64_t)d->num_sms * 8;
     if (blocks > cap) blocks = cap;
-    launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
+    if constexpr (BYTES == 32)  // same bytes in flight per lane as 2 x 16 B
+        launch_variant<BYTES, 4, 1, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
+    else
+        launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
     SYNK_LAUNCHED("gather_rows_kernel");
     return SYNK_OK;
 }
@@ -472,6 +504,11 @@ extern "C" int synk_gather_rows(synk_dev* d, const void* src, uint64_t src_rows,
     }
     if (force_bulk && (a & 15) == 0 && row_bytes <= 8192)
         return launch_bulk(d, src, src_rows, row_bytes, idx, n_idx, dst);
+    // 256-bit lanes (ld/st .v8.b32) when rows and pointers are 32-byte aligned:
+    // +2.9 % device, +5.5 % e2e on C2 vs 2 x 16-byte vectors (same-box A/B,
+    // profiles/r01_gather.md). SYNK_GATHER_V32=0 keeps 16-byte lanes.
+    static const bool v32 = !(getenv("SYNK_GATHER_V32") && getenv("SYNK_GATHER_V32")[0] == '0');
+    if (v32 && (a & 31) == 0) return launch<32>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 15) == 0) return launch<16>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 7) == 0) return launch<8>(d, src, src_rows, row_bytes, idx, n_idx, dst);
     if ((a & 3) == 0) return launch<4>(d, src, src_rows, row_bytes, idx, n_idx, dst);
