@@ -696,7 +696,7 @@ def ours(args, n_gpus, dist=None, world=1, local_device=0):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n_step * (2 * row_bytes + 8)),
                          "traffic_unit": "bytes/launch", "peak_kind": peak_kind,
-                         "kernel": "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
+                         "kernel": "gather_rows_kernel<32>" if row_bytes % 32 == 0 else "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
             "single_batch_us": 1e6 * hd["single_s"],
             "gather_from_host_memory": hd["host_source"],
             "gpu_launches": n_gpus * args.steps, "clocks": hd["clocks"], "setup_s": hd["setup_s"]}
