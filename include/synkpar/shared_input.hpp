@@ -64,6 +64,16 @@ public:
     const void* mirror_ptr(int device) const;
     // The mirror itself (bytes of the whole capacity), or an empty DevBuffer.
     DevBuffer mirror_buffer(int device) const;
+    // view() hands out a writable alias of the host store, which the HBM
+    // mirrors cannot observe. Once one has been taken while mirrors exist,
+    // the executor calls sync_mirrors() before the next call that reads
+    // them: the whole store is re-uploaded (and the mark cleared once no
+    // such view is alive any more), so writes through a view are seen just
+    // as in the reference, where the store is the only copy.
+    void sync_mirrors() const;
+    // The store as a read-only input (what view() returns, without marking
+    // the mirrors possibly stale): used by the executor and by copies.
+    NdBuffer store_view() const;
 
     struct Record;
 

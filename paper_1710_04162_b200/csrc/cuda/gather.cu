@@ -172,7 +172,15 @@ void launch_variant(synk_dev* d, unsigned blocks, const void* src, uint64_t src_
 template <int BYTES>
 int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
            const uint64_t* idx, uint64_t n_idx, void* dst) {
-    static const uint32_t chunk = getenv("SYNK_GATHER_ROWS") ? atoi(getenv("SYNK_GATHER_ROWS")) : 4;
+    // Rows per warp chunk (A/B knob): a multiple of the 4 rows in flight, at
+    // most one warp's worth of indices (lanes hold the chunk's indices).
+    static const uint32_t chunk = [] {
+        const char* e = getenv("SYNK_GATHER_ROWS");
+        long v = e ? strtol(e, nullptr, 10) : 4;
+        if (v < 4) v = 4;
+        if (v > 32) v = 32;
+        return (uint32_t)(v & ~3L);
+    }();
     // At most 8 CTAs of 8 warps per SM (about 2.7 waves at 3 resident
     // CTAs/SM: the oversubscription balances the random-row latency).
     // 4 rows x 2 vectors in flight per lane at <= 85 registers (3 CTAs/SM) won

@@ -82,6 +82,26 @@ void require_same_dtype(const detail::VarRecord& rec) {
         if (b.dtype() != rec.replicas[0].dtype()) throw DTypeError("combine_inplace: dtype mismatch across replicas");
 }
 
+// One Collective phase around an NCCL call per rank. A collective blocks its
+// rank until every peer has joined, so the ranks first meet on the host: a
+// rank whose pre-collective work throws aborts the rendezvous and its peers
+// fail with it (fail-stop, PhaseError of the lowest failing rank) instead of
+// waiting inside NCCL forever.
+template <class Enqueue>
+void nccl_phase(detail::PoolState& st, Enqueue&& enqueue) {
+    detail::PhaseRendezvous rv(st.world);
+    detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        try {
+            rv.arrive_and_wait();
+            enqueue(r);
+        } catch (...) {
+            rv.abort();
+            throw;
+        }
+        detail::dev_sync(st.ranks[r]);
+    });
+}
+
 } // namespace
 
 ReplicatedVariable replicate(WorkerPool& pool, const NdBuffer& init) {
@@ -121,9 +141,8 @@ void ReplicatedVariable::broadcast(std::size_t src) {
     std::vector<void*> ptrs = replica_ptrs(rec);
     const std::size_t bytes = s.byte_size();
     if (st.nccl) {  // library baseline backend (ForkOptions::collectives = "nccl")
-        detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        nccl_phase(st, [&](std::size_t r) {
             detail::check(synk_nccl_broadcast(st.handles[r], static_cast<int>(src), ptrs[r], bytes), "broadcast (nccl)");
-            detail::dev_sync(st.ranks[r]);
         });
         rec.coherent = true;
         return;
@@ -155,10 +174,9 @@ void ReplicatedVariable::all_reduce(ReduceOp op) {
     const std::size_t n = rec.replicas[0].size();
     const int dt = detail::synk_dtype(rec.replicas[0].dtype());
     if (st.nccl) {  // library baseline backend: NCCL's reduction order (within tolerance, not bitwise)
-        detail::run_pool_phase(st, PhaseKind::Collective, [&](std::size_t r) {
+        nccl_phase(st, [&](std::size_t r) {
             require_same_dtype(rec);
             detail::check(synk_nccl_all_reduce(st.handles[r], dt, detail::synk_op(op), ptrs[r], n), "all_reduce (nccl)");
-            detail::dev_sync(st.ranks[r]);
         });
         rec.coherent = true;
         return;

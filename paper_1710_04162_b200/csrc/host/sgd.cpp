@@ -285,7 +285,10 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
         if (st->nccl) {
             // Library baseline backend: NCCL all-reduce (sum, or avg = mean) of
             // this rank's gradient in place, then the rule on the reduced
-            // gradient -- NCCL synchronises the ranks on the device.
+            // gradient -- NCCL synchronises the ranks on the device. Meet on
+            // the host first: a rank that failed before this point aborts the
+            // rendezvous instead of stranding its peers inside the collective.
+            if (W > 1) rv.arrive_and_wait();
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &ma), "mark");
             if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
             if (r == 0) update_from_compute_end_ = false;

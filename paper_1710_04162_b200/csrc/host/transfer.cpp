@@ -3,6 +3,7 @@
 #include "transfer.hpp"
 
 #include <cstring>
+#include <vector>
 
 namespace synkpar::detail {
 
@@ -111,6 +112,22 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     } else if (const std::byte* dv = device_view(src.bytes())) {
         base = dv;  // gather straight out of pinned host memory over PCIe
     } else {
+        // Pageable source: gather the selected rows on the host and upload
+        // only those (not the whole source per rank per call); the rank's
+        // stream is drained before the temporary goes. An out-of-range index (possible only
+        // when the bounds check is deferred to the device) takes the device
+        // path instead, whose kernel flags it.
+        const std::uint64_t* list = sel.list + part.start;
+        bool in_range = true;
+        for (std::size_t i = 0; i < part.count() && in_range; ++i) in_range = list[i] < n_src;
+        if (in_range) {
+            std::vector<std::byte> rows(part.count() * row_bytes);
+            for (std::size_t i = 0; i < part.count(); ++i)
+                std::memcpy(rows.data() + i * row_bytes, src.bytes() + list[i] * row_bytes, row_bytes);
+            check(synk_copy(rd->h, out.data(), rows.data(), rows.size()), "excerpt: H2D gathered rows");
+            dev_sync(rd);
+            return out;
+        }
         staged = DevBuffer::alloc(rd, src.shape(), src.dtype());
         check(synk_copy(rd->h, staged.data(), src.bytes(), src.byte_size()), "excerpt: stage pageable source");
         base = staged.data();
