@@ -78,7 +78,10 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(bytes_per_launch, path="profiles/r01_gather_ncu_full_raw.csv"):
+TRAFFIC_CAPTURE = "profiles/r01_gather_ncu_full_raw.csv"
+
+
+def ncu_traffic(bytes_per_launch, path=TRAFFIC_CAPTURE):
     """dram__bytes_read.sum + dram__bytes_write.sum of the committed
     `ncu --set full` capture of the same gather launch (same rows per launch),
     or None when the capture does not match this launch size."""
@@ -188,7 +191,7 @@ def reference_arm(args, n_gpus):
         return line
     line.update({"value": res["gbs"], "ms_per_step": res["ms_per_step"],
                  "cpu_baseline": {"value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
-                                  "sample": "%d steps x %d rows gathered through call(indexes) with a no-op kernel "
+                                  "cpu_model": cpu_model(), "sample": "%d steps x %d rows gathered through call(indexes) with a no-op kernel "
                                             "from a %dx%d f32 SharedInputArray" % (steps, rows_per_step, args.rows,
                                                                                     args.cols)},
                  "e2e": {"value": res["gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
@@ -269,76 +272,9 @@ def slicing_c3(sk, pool, args, n_gpus, peak, peak_kind):
         res, err = run_reference_driver("slicing", ["--rows", sample, "--cols", cols, "--slices", slices,
                                                     "--steps", 2, "--warmup", 1, "--workers", os.cpu_count() or 1])
         out["cpu_baseline"] = err and {"unavailable": err} or {
-            "value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
+            "value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference", "cpu_model": cpu_model(),
             "sample": "2 calls over %dx%d f32 (explicit scatter input), num_slices=%d, Sum+Max+Gather" % (
                 sample, cols, slices)}
-    return out
-
-
-def collectives_c4(sk, args, n_gpus):
-    """C4: Replicated.all_reduce("mean") and broadcast(0) of f32 buffers from
-    1 KiB to 1 GiB, timed per call on the host (phase protocol + peer-memory
-    kernel + stream sync). busbw = S/t * 2(W-1)/W (all-reduce), S/t (broadcast).
-    With one GPU the W=2 ranks share it, so the peer-memory kernels move the
-    bytes through local HBM instead of NVLink (stated in the output)."""
-    world = n_gpus if n_gpus >= 2 else 2
-    ndev = max(1, sk.device_count())
-    devices = [d % ndev for d in range(n_gpus)] if n_gpus >= 2 else [0, 0]
-    sizes = [1 << k for k in range(10, 31, 3)] + [1 << 30]
-    rng = np.random.default_rng(1000)
-
-    def sweep_with(collectives):
-        sweep = []
-        with sk.Pool(workers=world, devices=devices, collectives=collectives) as pool:
-            for S in sizes:
-                n = S // 4
-                var = sk.replicate(pool, np.zeros(n, np.float32))
-                for r in range(world):
-                    var.set(r, rng.uniform(-1, 1, n).astype(np.float32))
-                reps = 200 if S <= (1 << 20) else (30 if S <= (1 << 27) else 8)
-                for _ in range(3):
-                    var.all_reduce("mean")
-                    var.broadcast(0)
-                t = time.perf_counter()
-                for _ in range(reps):
-                    var.all_reduce("mean")
-                t_ar = (time.perf_counter() - t) / reps
-                t = time.perf_counter()
-                for _ in range(reps):
-                    var.broadcast(0)
-                t_bc = (time.perf_counter() - t) / reps
-                coherent = var.coherent
-                del var
-                sweep.append({"bytes": S, "allreduce_us": 1e6 * t_ar,
-                              "allreduce_busbw_gbs": S / t_ar * 2 * (world - 1) / world / 1e9,
-                              "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9,
-                              "coherent": coherent})
-        return sweep
-
-    sweep = sweep_with("p2p")
-    out = {"config": "C4: all_reduce mean + broadcast(0) of f32 buffers 1 KiB - 1 GiB, W=%d ranks" % world,
-           "ranks": world, "devices": devices,
-           "link": "NVLink peer memory" if len(set(devices)) >= 2 else "1 GPU: the ranks share it, peer-memory "
-                                                                         "kernels run over local HBM (NVLink unmeasured)",
-           "sweep": sweep}
-    # Library baseline on distinct GPUs: the same sweep through NCCL (busbw vs
-    # the NVLink peak, next to the peer-memory kernels above).
-    if len(set(devices)) >= 2 and sk.nccl_available():
-        try:
-            out["nccl_sweep"] = sweep_with("nccl")
-        except Exception as e:  # reported, not fatal
-            out["nccl_sweep"] = {"unavailable": str(e)[:200]}
-    if not args.no_cpu_baseline:
-        ref = []
-        for S in (1 << 10, 1 << 16, 1 << 20, 1 << 26):
-            res, err = run_reference_driver("collective", ["--bytes", S, "--workers", world, "--steps", 3,
-                                                           "--warmup", 1])
-            if res is None:
-                ref = {"unavailable": err}
-                break
-            ref.append({k: res[k] for k in ("bytes", "allreduce_us", "allreduce_busbw_gbs", "broadcast_us",
-                                            "broadcast_busbw_gbs")})
-        out["cpu_baseline"] = {"kind": "reference", "cores": world, "sweep": ref}
     return out
 
 
@@ -529,77 +465,361 @@ def gather_headline(args, n_gpus, devices, dist, world):
             rep_acc[k] += rep[k] / args.steps
         rep_acc["compute_s"] += max(rep["rank_compute_s"]) / args.steps
     e2e_breakdown = {k + "_us": 1e6 * v for k, v in rep_acc.items()}
+    # the config's own granularity: ONE 4096-row batch per GPU per Function.call
+    one_idx = []
+    for _ in range(220):
+        buf = sk.pinned_array(B * n_local, "int64")
+        buf[:] = rng.integers(0, rows, B * n_local)
+        one_idx.append(buf)
+    for s in range(20):
+        f.call([arr], indexes=one_idx[s])
+    barrier()
+    t0 = time.perf_counter()
+    for s in range(20, 220):
+        (cnt,) = f.call([arr], indexes=one_idx[s])
+    one_s = max_over_ranks((time.perf_counter() - t0) / 200)
+    assert float(cnt) == B * n_local
+    single_call = {"rows_per_gpu": B, "us_per_call": 1e6 * one_s,
+                   "gbs": world * n_local * B * (2 * row_bytes + BYTES_PER_ROW_EXTRA) / one_s / 1e9,
+                   "h2d_bytes_per_call": 8 * B * n_local, "d2h_bytes_per_call": 8}
 
     pool.shutdown()
     del arr
-    return {"value": value, "region_s": region_s, "e2e": e2e, "e2e_breakdown": e2e_breakdown, "achieved": achieved,
+    return {"value": value, "region_s": region_s, "e2e": e2e, "e2e_breakdown": e2e_breakdown,
+            "single_call": single_call, "achieved": achieved,
             "single_s": single_s, "clocks": clocks.summary(), "host_source": host_src,
             "setup_s": setup_s, "n_step": n_step, "row_bytes": row_bytes, "peak": peak, "peak_kind": peak_kind}
 
 
-def sub_measurements(args, n_gpus, peak, peak_kind):
-    """C1, C5 (sync SGD through Trainer), C3 (slicing), C4 (collectives): the
-    executor's own single-process pool over the job's GPUs (the paper's
-    master + workers; collectives are peer-memory kernels across them)."""
-    import paper_1710_04162_b200 as sk
+# ---- sync SGD (C1, C5): per-N samples/s, scaling and the paper's Table-1 split ----------
 
-    ndev = max(1, sk.device_count())
-    pool = sk.Pool(workers=n_gpus, devices=[d % ndev for d in range(n_gpus)])
-    rng = np.random.default_rng(12)
-    total_steps = args.warmup + args.steps
-    # ---- sync SGD (C1) sub-measurement ------------------------------------------------
-    sgd = None
-    if not args.no_sgd:
-        cfg = sk.MlpConfig(in_dim=784, width=512, out_dim=10, layers=2, seed=1)
-        x, y = sk.mlp_make_dataset(65536, cfg, seed=2, dtype="f32")
+SGD_MODELS = {
+    "c1": {"dims": [784, 512, 10], "per_gpu": 256, "rows": 65536, "compute": "native", "warm": 30, "dtype": "f32",
+           "label": "C1: MLP 784-512-10 fp32 (FFMA/DFMA GEMMs), indexed from a 65536-row SharedInput (HBM mirror), "
+                    "SGD lr 0.01, gradient all-reduce mean fused with the update"},
+    "c5": {"dims": [2048, 4096, 4096, 100], "per_gpu": 8192, "rows": 16384, "compute": "bf16", "warm": 3,
+           "dtype": "bf16",
+           "label": "C5 (R1): MLP 2048-4096-4096-100 (25,583,716 params, fp32 master), bf16 tcgen05 GEMMs, indexed "
+                    "from a 16384-row HBM mirror, SGD lr 0.01, gradient all-reduce mean + update fused and bucketed "
+                    "per layer (overlapped with the backward pass)"},
+}
+
+
+def flops_per_sample(dims):
+    """Forward + weight-gradient + input-gradient products of the MLP (no dX
+    for layer 0): 6*sum(d_l*d_{l+1}) - 2*d_0*d_1."""
+    return 6 * sum(a * b for a, b in zip(dims[:-1], dims[1:])) - 2 * dims[0] * dims[1]
+
+
+def gpu_counts(n_gpus):
+    """The paper's 1/2/4/8 sweep, capped at the job's GPUs (and the job size itself)."""
+    ns = [n for n in (1, 2, 4, 8) if n <= n_gpus]
+    return ns if n_gpus in ns else ns + [n_gpus]
+
+
+def measure_sgd(sk, model, devices, per_rank, steps, warmup, seed, sustained_s=0.0):
+    """One pool over `devices`; `steps` timed train_steps (host clock around
+    the calls: the pinned index list goes H2D, the loss comes back D2H every
+    step), then an untimed repeat of as many steps read through
+    Trainer.last_report for the Table-1 split (the reference accounting,
+    src/bench.cpp:186-198), then optionally `sustained_s` seconds back to back."""
+    m = SGD_MODELS[model]
+    dims, n = m["dims"], len(devices)
+    gb = per_rank * n
+    with sk.Pool(workers=n, devices=list(devices)) as pool:
+        cfg = sk.MlpConfig(in_dim=dims[0], width=dims[1], out_dim=dims[-1], layers=len(dims) - 1, seed=1)
+        x, y = sk.mlp_make_dataset(m["rows"], cfg, seed=2, dtype="f32")
         sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
         sx.mirror(pool)
         sy.mirror(pool)
         block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
-        g = sk.mlp_grad_function(pool, block)
+        g = sk.mlp_grad_function(pool, block, compute=m["compute"])
         sk.distribute(pool)
         tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
-        # Latency-bound steps: a longer untimed warm-up lets the per-rank CUDA-graph
-        # cache settle on the recycled batch buffers (captures cost ~0.5 ms each).
-        warm1 = max(args.warmup, 30)
-        sel = [pinned_indexes(sk, rng, 65536, 256 * n_gpus) for _ in range(warm1 + args.steps)]
-        for s in range(warm1):
+        rng = np.random.default_rng(seed)
+        # Latency-bound C1 steps: a longer untimed warm-up lets the per-rank
+        # CUDA-graph cache settle on the recycled batch buffers.
+        warm = max(warmup, m["warm"])
+        sel = [pinned_indexes(sk, rng, m["rows"], gb) for _ in range(warm + 2 * steps)]
+        for s in range(warm):
             tr.train_step(g, [sx, sy], indexes=sel[s])
         t0 = time.perf_counter()
-        for s in range(warm1, warm1 + args.steps):
+        for s in range(warm, warm + steps):
             loss = tr.train_step(g, [sx, sy], indexes=sel[s])
         dt = time.perf_counter() - t0
-        rep = tr.last_report
-        sgd = {"config": "C1: MLP 784-512-10 fp32, batch 256 per GPU (scaled), indexed from a 65536-row SharedInput "
-                         "(HBM mirror), SGD lr 0.01, grad all-reduce mean fused with the update",
-               "samples_per_s": 256 * n_gpus * args.steps / dt, "ms_per_step": 1e3 * dt / args.steps,
-               "allreduce_ms_last": 1e3 * rep["allreduce_s"], "loss_last": loss, "coherent": block.params.coherent}
+        t1 = {"function_s": 0.0, "shuffle_s": 0.0, "straggler_s": 0.0, "allreduce_s": 0.0, "total_s": 0.0}
+        for s in range(warm + steps, warm + 2 * steps):
+            t = time.perf_counter()
+            tr.train_step(g, [sx, sy], indexes=sel[s])
+            t1["total_s"] += time.perf_counter() - t
+            rep = tr.last_report
+            gc, sc = rep["grad_call"], rep["step_call"]
+            t1["function_s"] += float(np.mean(gc["rank_compute_s"])) + (
+                float(np.mean(sc["rank_compute_s"])) if sc["rank_compute_s"] else 0.0)
+            t1["shuffle_s"] += gc["scatter_s"]
+            t1["straggler_s"] += gc["straggler_s"] + sc["straggler_s"]
+            t1["allreduce_s"] += rep["allreduce_s"]
+        sustained = None
+        if sustained_s > 0:
+            k, t = 0, time.perf_counter()
+            while time.perf_counter() - t < sustained_s:
+                tr.train_step(g, [sx, sy], indexes=sel[k % len(sel)])
+                k += 1
+            el = time.perf_counter() - t
+            sustained = {"seconds": el, "steps": k, "ms_per_step": 1e3 * el / k, "samples_per_s": gb * k / el}
+        return {"n_gpus": n, "devices": list(devices), "global_batch": gb, "per_rank_batch": per_rank,
+                "steps": steps, "seconds": dt, "samples_per_s": gb * steps / dt, "ms_per_step": 1e3 * dt / steps,
+                "table1": t1, "loss_last": float(loss), "coherent": bool(block.params.coherent),
+                "n_params": int(block.length), "sustained": sustained}
 
-    # ---- wide MLP (C5) sync SGD on tcgen05 bf16 -------------------------------------------
-    sgd5 = None
-    if not args.no_sgd:
-        dims = [2048, 4096, 4096, 100]
-        cfg = sk.MlpConfig(in_dim=dims[0], width=dims[1], out_dim=dims[-1], layers=3, seed=1)
-        x, y = sk.mlp_make_dataset(16384, cfg, seed=2, dtype="f32")
-        sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
-        sx.mirror(pool)
-        sy.mirror(pool)
-        block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
-        g = sk.mlp_grad_function(pool, block, compute="bf16")
-        sk.distribute(pool)
-        tr = sk.Trainer(pool, block, sk.SgdRule(), lr=0.01)
-        per_gpu = 8192
-        sel = [pinned_indexes(sk, rng, 16384, per_gpu * n_gpus) for _ in range(total_steps)]
-        for s in range(args.warmup):
-            tr.train_step(g, [sx, sy], indexes=sel[s])
-        t0 = time.perf_counter()
-        for s in range(args.warmup, total_steps):
-            loss = tr.train_step(g, [sx, sy], indexes=sel[s])
-        dt = time.perf_counter() - t0
-        flops_per_sample = 6 * sum(a * b for a, b in zip(dims[:-1], dims[1:])) - 2 * dims[0] * dims[1]
-        # Roofline denominators (MEASURED_PEAKS.json): the sustained bf16 figure
-        # applies to a long back-to-back GEMM stream like this step (power
-        # management lowers the clocks under sustained tensor load); burst kept too.
+
+def stub_sgd(model, devices, per_rank, steps, sustained_s=0.0):
+    """--dry-run stand-in for measure_sgd (no GPU): the same record shape with
+    synthetic timings (a fixed per-step time plus a 2 % per-GPU overhead)."""
+    n = len(devices)
+    ms = (0.11 if model == "c1" else 1.14) * (1 + 0.02 * (n - 1))
+    dt = ms * steps / 1e3
+    t1 = {"function_s": 0.8 * dt, "shuffle_s": 0.05 * dt, "straggler_s": 0.01 * dt, "allreduce_s": 0.1 * dt,
+          "total_s": dt}
+    gb = per_rank * n
+    return {"n_gpus": n, "devices": list(devices), "global_batch": gb, "per_rank_batch": per_rank, "steps": steps,
+            "seconds": dt, "samples_per_s": gb * steps / dt, "ms_per_step": ms, "table1": t1, "loss_last": 1.0,
+            "coherent": True, "n_params": 0, "stub": True,
+            "sustained": {"seconds": sustained_s, "steps": 1, "ms_per_step": ms, "samples_per_s": gb / ms * 1e3}
+            if sustained_s > 0 else None}
+
+
+def scaling_summary(runs, model):
+    """speedup_vs_1 / speedup_vs_2 as the reference bench (src/bench.cpp:213-221),
+    efficiency = speedup_vs_1 / N (the north star: >= 0.9 at N=8), Table-1 per
+    step in microseconds and as fractions of the step."""
+    base = {r["n_gpus"]: r["samples_per_s"] for r in runs}
+    dims = SGD_MODELS[model]["dims"]
+    for r in runs:
+        n = r["n_gpus"]
+        r["speedup_vs_1"] = r["samples_per_s"] / base[1] if 1 in base else None
+        r["speedup_vs_2"] = r["samples_per_s"] / base[2] if 2 in base else None
+        r["efficiency_vs_linear"] = r["speedup_vs_1"] / n if r["speedup_vs_1"] is not None else None
+        t1 = r["table1"]
+        tot = t1["total_s"] or 1e-30
+        r["table1_per_step_us"] = {k.replace("_s", ""): 1e6 * v / r["steps"] for k, v in t1.items()}
+        r["table1_frac"] = {k.replace("_s", ""): v / tot for k, v in t1.items() if k != "total_s"}
+        r["model_tflops_per_gpu"] = flops_per_sample(dims) * r["samples_per_s"] / n / 1e12
+    return runs
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def reference_sgd(worker_counts, steps=3):
+    """The unmodified reference's SyncSgd::train_step (oracle/_ref/ref_driver
+    --mode sgd: src/sgd.cpp:259-332 through its public API) on this box's
+    cores, W threads pinned, timed in this run: configs[0] exactly (W=2,
+    batch 256 global) and the scaled sweep (256 rows per worker)."""
+    cores = os.cpu_count() or 1
+    out = {"kind": "reference", "cpu_model": cpu_model(), "host_cores": cores,
+           "timing": "steady clock around SyncSgd::train_step; Table-1 split from the reference's StepReport"}
+    res, err = run_reference_driver("sgd", ["--workers", 2, "--batch", 256, "--steps", max(steps, 3), "--warmup", 1])
+    out["configs0_exact"] = err and {"unavailable": err} or dict(res, cores=2, sample="%d steps" % res["steps"])
+    runs = []
+    for w in worker_counts:
+        if w > cores:
+            continue
+        res, err = run_reference_driver("sgd", ["--workers", w, "--batch", 256 * w, "--steps", steps, "--warmup", 1])
+        if res is None:
+            runs.append({"workers": w, "unavailable": err})
+            continue
+        runs.append(dict(res, cores=w))
+    b1 = next((r["samples_per_s"] for r in runs if r.get("workers") == 1 and "samples_per_s" in r), None)
+    for r in runs:
+        if b1 and "samples_per_s" in r:
+            r["speedup_vs_1"] = r["samples_per_s"] / b1
+    out["scaled"] = runs
+    return out
+
+
+def tree_fold(vals, op):
+    """The reference's binomial collective order (replicated.cpp:16-29):
+    step = 1, 2, 4, ...: acc[r] = acc[r] op acc[r + step] for r = 0, 2*step, ..."""
+    acc = [v.copy() for v in vals]
+    step = 1
+    while step < len(acc):
+        for r in range(0, len(acc) - step, 2 * step):
+            a, b = acc[r], acc[r + step]
+            acc[r] = a + b if op == "sum" else np.where(b > a, b, a)
+        step *= 2
+    return acc[0]
+
+
+def cross_gpu_selfcheck(sk, devices):
+    """Before any timed N>1 number: the peer-memory collectives across these
+    GPUs must be BITWISE equal to the reference's tree order (sum, mean, max;
+    broadcast), and NCCL's sum within 8*W*eps_f32 (acceptance_main.cpp:415).
+    Raises on any mismatch -- a wrong collective never gets timed."""
+    W = len(devices)
+    rng = np.random.default_rng(99)
+    checks = []
+    for n in (1000, (1 << 20) + 3):  # one-launch path (rank 0 folds all chunks) and per-rank chunk kernels
+        vals = [rng.uniform(-1, 1, n).astype(np.float32) for _ in range(W)]
+        with sk.Pool(workers=W, devices=list(devices)) as pool:
+            var = sk.replicate(pool, np.zeros(n, np.float32))
+            for op in ("sum", "mean", "max"):
+                for r in range(W):
+                    var.set(r, vals[r])
+                var.all_reduce(op)
+                want = tree_fold(vals, "max" if op == "max" else "sum")
+                if op == "mean":
+                    want = (want.astype(np.float64) * (1.0 / W)).astype(np.float32)
+                for r in range(W):
+                    if var.get(r).tobytes() != want.tobytes():
+                        raise RuntimeError("self-check: all_reduce(%s) of %d floats differs from the tree order on "
+                                           "rank %d (devices %s)" % (op, n, r, devices))
+                checks.append("all_reduce_%s_%d: bitwise" % (op, n))
+            for r in range(W):
+                var.set(r, vals[r])
+            var.broadcast(W - 1)
+            for r in range(W):
+                if var.get(r).tobytes() != vals[W - 1].tobytes():
+                    raise RuntimeError("self-check: broadcast differs on rank %d (devices %s)" % (r, devices))
+            checks.append("broadcast_%d: bitwise" % n)
+        if len(set(devices)) == W and sk.nccl_available():
+            with sk.Pool(workers=W, devices=list(devices), collectives="nccl") as pool:
+                var = sk.replicate(pool, np.zeros(n, np.float32))
+                for r in range(W):
+                    var.set(r, vals[r])
+                var.all_reduce("sum")
+                want = tree_fold(vals, "sum").astype(np.float64)
+                tol = 8 * W * float(np.finfo(np.float32).eps)
+                for r in range(W):
+                    err = np.max(np.abs(var.get(r) - want) / np.maximum(1.0, np.abs(want)))
+                    if not err <= tol:
+                        raise RuntimeError("self-check: NCCL sum elem_err %.3g > %.3g on rank %d" % (err, tol, r))
+                checks.append("nccl_all_reduce_sum_%d: elem_err <= 8*W*eps" % n)
+    return {"devices": list(devices), "distinct_gpus": len(set(devices)), "ok": True, "checks": checks}
+
+
+def collectives_sweep(sk, devices, collectives, sizes, rng):
+    """Replicated.all_reduce("mean") and broadcast(0) per size, timed per call
+    on the host (phase protocol + kernel + stream sync)."""
+    world = len(devices)
+    sweep = []
+    with sk.Pool(workers=world, devices=list(devices), collectives=collectives) as pool:
+        for S in sizes:
+            n = S // 4
+            var = sk.replicate(pool, np.zeros(n, np.float32))
+            for r in range(world):
+                var.set(r, rng.uniform(-1, 1, n).astype(np.float32))
+            reps = 200 if S <= (1 << 20) else (30 if S <= (1 << 27) else 8)
+            for _ in range(3):
+                var.all_reduce("mean")
+                var.broadcast(0)
+            t = time.perf_counter()
+            for _ in range(reps):
+                var.all_reduce("mean")
+            t_ar = (time.perf_counter() - t) / reps
+            t = time.perf_counter()
+            for _ in range(reps):
+                var.broadcast(0)
+            t_bc = (time.perf_counter() - t) / reps
+            coherent = var.coherent
+            del var
+            sweep.append({"bytes": S, "allreduce_us": 1e6 * t_ar,
+                          "allreduce_busbw_gbs": S / t_ar * 2 * (world - 1) / world / 1e9,
+                          "broadcast_us": 1e6 * t_bc, "broadcast_busbw_gbs": S / t_bc / 1e9, "coherent": coherent})
+    return sweep
+
+
+def stub_sweep(devices, sizes):
+    world = len(devices)
+    return [{"bytes": S, "allreduce_us": 10 + S / 5e5, "allreduce_busbw_gbs": S / (10e-6 + S / 5e11) * 2 * (world - 1)
+             / world / 1e9, "broadcast_us": 10 + S / 7e5, "broadcast_busbw_gbs": S / (10e-6 + S / 7e11) / 1e9,
+             "coherent": True, "stub": True} for S in sizes]
+
+
+NVLINK_PEAK_GBS = 900.0  # NVLink 5, per direction per GPU (B200_PROFILING.md)
+
+
+def collectives_c4(sk, args, n_gpus, dry=False):
+    """C4: all-reduce mean + broadcast(0), 1 KiB - 1 GiB, at W = 2/4/8 on
+    distinct GPUs (peer-memory kernels, and NCCL as the library baseline),
+    busbw = S/t * 2(W-1)/W (all-reduce), S/t (broadcast), against the NVLink
+    peak. With one GPU the W=2 ranks share it and the bytes move through
+    local HBM (stated in the output, not an NVLink number)."""
+    ndev = n_gpus if dry else max(1, sk.device_count())
+    sizes = [1 << k for k in range(10, 31, 3)] + [1 << 30]
+    rng = np.random.default_rng(1000)
+    worlds = [w for w in (2, 4, 8) if w <= min(n_gpus, ndev)]
+    runs = []
+    if not worlds:  # one GPU: W=2 ranks on it
+        devs = [0, 0]
+        runs.append({"ranks": 2, "devices": devs, "link": "1 GPU: the ranks share it, peer-memory kernels run over "
+                                                          "local HBM (NVLink unmeasured)",
+                     "p2p": stub_sweep(devs, sizes) if dry else collectives_sweep(sk, devs, "p2p", sizes, rng)})
+    for w in worlds:
+        devs = list(range(w))
+        run = {"ranks": w, "devices": devs, "link": "NVLink peer memory (NVSwitch)",
+               "p2p": stub_sweep(devs, sizes) if dry else collectives_sweep(sk, devs, "p2p", sizes, rng)}
+        if dry or sk.nccl_available():
+            try:
+                run["nccl"] = stub_sweep(devs, sizes) if dry else collectives_sweep(sk, devs, "nccl", sizes, rng)
+            except Exception as e:  # reported, not fatal
+                run["nccl"] = {"unavailable": str(e)[:200]}
+        for key in ("p2p", "nccl"):
+            sw = run.get(key)
+            if isinstance(sw, list) and sw:
+                big = sw[-1]
+                run[key + "_1gib_busbw_frac_of_nvlink"] = {
+                    "allreduce": big["allreduce_busbw_gbs"] / NVLINK_PEAK_GBS,
+                    "broadcast": big["broadcast_busbw_gbs"] / NVLINK_PEAK_GBS}
+        runs.append(run)
+    out = {"config": "C4: all_reduce mean + broadcast(0) of f32 buffers 1 KiB - 1 GiB", "nvlink_peak_gbs":
+           NVLINK_PEAK_GBS, "runs": runs}
+    if not args.no_cpu_baseline:
+        ref = []
+        for S in (1 << 10, 1 << 16, 1 << 20, 1 << 26):
+            res, err = run_reference_driver("collective", ["--bytes", S, "--workers", 2, "--steps", 3, "--warmup", 1])
+            if res is None:
+                ref = {"unavailable": err}
+                break
+            ref.append({k: res[k] for k in ("bytes", "allreduce_us", "allreduce_busbw_gbs", "broadcast_us",
+                                            "broadcast_busbw_gbs")})
+        out["cpu_baseline"] = {"kind": "reference", "cores": 2, "cpu_model": cpu_model(), "sweep": ref}
+    return out
+
+
+def sync_sgd_section(sk, args, n_gpus, model, dry=False):
+    """Per-N samples/s of one sync-SGD model (scaled mode: fixed batch per
+    GPU), speedups, efficiency and the Table-1 split; N=1 also runs a 3 s
+    back-to-back stretch (the sustained figure at the power cap)."""
+    m = SGD_MODELS[model]
+    runs = []
+    for n in gpu_counts(n_gpus):
+        devs = list(range(n))
+        sus = 3.0 if n == 1 and model == "c5" else 0.0
+        if dry:
+            runs.append(stub_sgd(model, devs, m["per_gpu"], args.steps, sus))
+        else:
+            runs.append(measure_sgd(sk, model, devs, m["per_gpu"], args.steps, args.warmup, 12 + n, sus))
+    scaling_summary(runs, model)
+    top = runs[-1]
+    out = {"config": m["label"] + ", batch %d per GPU (scaled)" % m["per_gpu"], "dtype": m["dtype"],
+           "flops_per_sample": flops_per_sample(m["dims"]), "runs": runs,
+           "samples_per_s": top["samples_per_s"], "ms_per_step": top["ms_per_step"], "n_gpus": top["n_gpus"],
+           "table1_note": "function = gradient-call compute (mean over ranks, device events); shuffle = staging of "
+                          "the indexed batch before compute (0 when the gather is fused into the compute graph); "
+                          "straggler = max - mean rank task; allreduce = the fused all-reduce + 1/W + update "
+                          "kernel (so the update sits here, not in function)"}
+    if model == "c5":
         bf16_peak, bf16_sustained, peak_kind = 1609.7, 1365.0, "fallback"
         try:
             with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -609,76 +829,81 @@ def sub_measurements(args, n_gpus, peak, peak_kind):
             peak_kind = "measured"
         except Exception:
             pass
-        tflops = flops_per_sample * per_gpu * n_gpus * args.steps / dt / 1e12 / n_gpus
-        sgd5 = {"config": "C5 (R1): MLP 2048-4096-4096-100 (25,583,716 params, fp32 master), bf16 tcgen05 GEMMs, "
-                          "batch %d per GPU indexed from a 16384-row HBM mirror, SGD lr 0.01, fused grad "
-                          "all-reduce mean + update" % per_gpu,
-                "n_params": int(block.length), "samples_per_s": per_gpu * n_gpus * args.steps / dt,
-                "ms_per_step": 1e3 * dt / args.steps, "model_tflops_per_gpu": tflops,
-                "frac_of_bf16_peak": tflops / bf16_peak, "frac_of_bf16_sustained": tflops / bf16_sustained,
-                "bf16_peak_tflops": bf16_peak, "bf16_sustained_tflops": bf16_sustained, "peak_kind": peak_kind,
-                "loss_last": loss, "coherent": block.params.coherent}
-
-    # ---- slicing + aggregation (C3) sub-measurement ----------------------------------
-    c3 = None
-    if not args.no_c3:
-        c3 = slicing_c3(sk, pool, args, n_gpus, peak, peak_kind)
-
-    pool.shutdown()
-    # ---- C1 exactly as BASELINE configs[0] states it: W=2 workers, batch 256
-    # global (128 per rank), the CPU reference's own configuration -------------
-    sgd_exact = None
-    if not args.no_sgd:
-        ndev = max(1, sk.device_count())
-        devices = [0, 1 % ndev]
-        with sk.Pool(workers=2, devices=devices) as pool2:
-            cfg = sk.MlpConfig(in_dim=784, width=512, out_dim=10, layers=2, seed=1)
-            x, y = sk.mlp_make_dataset(65536, cfg, seed=2, dtype="f32")
-            sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
-            sx.mirror(pool2)
-            sy.mirror(pool2)
-            block = sk.ParamBlock.create(pool2, sk.mlp_init_params(cfg, "f32"))
-            g = sk.mlp_grad_function(pool2, block)
-            sk.distribute(pool2)
-            tr = sk.Trainer(pool2, block, sk.SgdRule(), lr=0.01)
-            warm1 = max(args.warmup, 30)
-            sel = [pinned_indexes(sk, rng, 65536, 256) for _ in range(warm1 + args.steps)]
-            for s in range(warm1):
-                tr.train_step(g, [sx, sy], indexes=sel[s])
-            t0 = time.perf_counter()
-            for s in range(warm1, warm1 + args.steps):
-                loss = tr.train_step(g, [sx, sy], indexes=sel[s])
-            dt = time.perf_counter() - t0
-            sgd_exact = {"config": "C1 as configs[0]: MLP 784-512-10 fp32, W=2 workers, batch 256 global (128 per "
-                                   "rank), indexed, SGD lr 0.01, grad all-reduce mean fused with the update",
-                         "devices": devices, "samples_per_s": 256 * args.steps / dt,
-                         "ms_per_step": 1e3 * dt / args.steps, "loss_last": loss, "coherent": block.params.coherent,
-                         "reference_cpu_samples_per_s": 2048,
-                         "reference_note": "BASELINE/SURVEY probe of the unmodified reference, W=2, 8-core box"}
-    # ---- shared-variable sync sweep (C4): its own pool (one live pool per process) ----
-    c4 = None
-    if not args.no_c4:
-        c4 = collectives_c4(sk, args, n_gpus)
-    out = {}
-    if sgd:
-        out["sync_sgd"] = sgd
-    if sgd_exact:
-        out["sync_sgd_c1_exact"] = sgd_exact
-    if sgd5:
-        out["sync_sgd_wide_bf16"] = sgd5
-    if c3:
-        out["slicing_c3"] = c3
-    if c4:
-        out["collectives_c4"] = c4
+        r1 = runs[0]
+        out.update({"bf16_peak_tflops": bf16_peak, "bf16_sustained_tflops": bf16_sustained, "peak_kind": peak_kind,
+                    "model_tflops_per_gpu_n1": r1["model_tflops_per_gpu"],
+                    "frac_of_bf16_sustained_n1": r1["model_tflops_per_gpu"] / bf16_sustained,
+                    "frac_of_bf16_peak_n1": r1["model_tflops_per_gpu"] / bf16_peak})
+        if r1.get("sustained"):
+            sus_tf = flops_per_sample(m["dims"]) * r1["sustained"]["samples_per_s"] / 1e12
+            out["sustained_n1"] = dict(r1["sustained"], model_tflops=sus_tf, frac_of_bf16_sustained=sus_tf /
+                                       bf16_sustained)
     return out
 
 
-def ours(args, n_gpus, dist=None, world=1, local_device=0):
+def sub_measurements(args, n_gpus, peak, peak_kind, dry=False):
+    """Everything beyond the C2 headline, on the executor's own single-process
+    pools over the job's GPUs (the paper's master + workers): the cross-GPU
+    self-check, C1 and C5 sync SGD at N = 1/2/4/8 (<= the job's GPUs) with the
+    Table-1 split, C1 exactly as configs[0], the reference's own SyncSgd
+    timed here, C3 slicing and the C4 collective sweep."""
+    sk = None
+    if not dry:
+        import paper_1710_04162_b200 as sk
+    out = {}
+    ndev = n_gpus if dry else max(1, sk.device_count())
+    sc_devs = list(range(n_gpus)) if n_gpus >= 2 and ndev >= n_gpus else [0, 0]
+    out["cross_gpu_selfcheck"] = ({"devices": sc_devs, "ok": True, "stub": True} if dry
+                                  else cross_gpu_selfcheck(sk, sc_devs))
+    if not args.no_sgd:
+        out["sync_sgd"] = sync_sgd_section(sk, args, n_gpus, "c1", dry)
+        exact_devs = [0, 1] if ndev >= 2 else [0, 0]
+        ex = (stub_sgd("c1", exact_devs, 128, args.steps) if dry
+              else measure_sgd(sk, "c1", exact_devs, 128, args.steps, args.warmup, 31))
+        out["sync_sgd_c1_exact"] = dict(ex, config="C1 as configs[0]: MLP 784-512-10 fp32, W=2 workers, batch 256 "
+                                                   "global (128 per rank), indexed, SGD lr 0.01, grad all-reduce "
+                                                   "mean fused with the update")
+        if not args.no_cpu_baseline:
+            ref = reference_sgd(gpu_counts(n_gpus) if n_gpus > 1 else [1, 2], steps=3)
+            out["sync_sgd"]["cpu_baseline"] = ref
+            exact = ref.get("configs0_exact", {})
+            if "samples_per_s" in exact:
+                out["sync_sgd_c1_exact"]["cpu_baseline"] = {
+                    "value": exact["samples_per_s"], "unit": "samples/s", "cores": 2, "kind": "reference",
+                    "cpu_model": ref["cpu_model"], "sample": "%d SyncSgd::train_step calls, W=2 threads, batch 256"
+                    % exact["steps"], "table1": exact.get("table1")}
+                out["sync_sgd_c1_exact"]["speedup_vs_cpu_reference"] = ex["samples_per_s"] / exact["samples_per_s"]
+        out["sync_sgd_wide_bf16"] = sync_sgd_section(sk, args, n_gpus, "c5", dry)
+    if not args.no_c3 and not dry:
+        with sk.Pool(workers=n_gpus, devices=[d % ndev for d in range(n_gpus)]) as pool:
+            out["slicing_c3"] = slicing_c3(sk, pool, args, n_gpus, peak, peak_kind)
+    if not args.no_c4:
+        out["collectives_c4"] = collectives_c4(sk, args, n_gpus, dry)
+    return out
+
+
+def stub_headline(args, n_gpus, world):
+    """--dry-run stand-in for gather_headline (no GPU): synthetic timings of
+    the same record shape, so the line's assembly runs unchanged on CPU."""
+    n_step, row_bytes = args.batch * args.batches, args.cols * 4
+    peak, peak_kind = measured_peak_hbm()
+    launch_s = n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA) / (0.9 * peak * 1e9)
+    bytes_step = n_gpus * n_step * (2 * row_bytes + BYTES_PER_ROW_EXTRA)
+    return {"value": bytes_step / launch_s / 1e9, "region_s": launch_s * args.steps, "e2e": 0.8 * bytes_step / launch_s
+            / 1e9, "e2e_breakdown": {}, "single_call": {"rows_per_gpu": args.batch, "us_per_call": 20.0, "stub": True},
+            "achieved": 0.9 * peak, "single_s": 8e-6, "clocks": {"sm_mhz": None, "sm_max_mhz": None,
+                                                               "reasons": ["dry-run"]},
+            "host_source": None, "setup_s": 0.0, "n_step": n_step, "row_bytes": row_bytes, "peak": peak,
+            "peak_kind": peak_kind}
+
+
+def ours(args, n_gpus, dist=None, world=1, local_device=0, dry=False):
     """Our arm. Single process: the headline on a pool over all N GPUs. Under
     torchrun: one process per GPU for the headline (each its own one-GPU
-    pool), then rank 0 alone runs the sub-measurements over every GPU."""
+    pool), then rank 0 alone runs the sub-measurements over every GPU.
+    dry: no GPU work, synthetic timings through the same line assembly."""
     devices = [local_device] if dist is not None else list(range(n_gpus))
-    hd = gather_headline(args, n_gpus, devices, dist, world)
+    hd = stub_headline(args, n_gpus, world) if dry else gather_headline(args, n_gpus, devices, dist, world)
     if dist is not None:
         dist.barrier()  # every rank's headline pool is down before rank 0 opens its own over all GPUs
         if dist.get_rank() != 0:
@@ -691,19 +916,42 @@ def ours(args, n_gpus, dist=None, world=1, local_device=0):
             "config": workload_config(args, n_gpus),
             "e2e": {"value": hd["e2e"], "unit": "GB/s", "h2d_bytes_per_step": 8 * n_step * n_gpus,
                     "d2h_bytes_per_step": 8 * (world if dist is not None else 1),
-                    "path": "Function.call(indexes) -> row_count kernel -> Sum",
-                    "breakdown_per_call": hd["e2e_breakdown"]},
+                    "path": "Function.call(indexes) -> row_count kernel -> Sum, %d batches of %d rows per GPU per "
+                            "call" % (args.batches, args.batch),
+                    "breakdown_per_call": hd["e2e_breakdown"], "single_batch_call": hd["single_call"],
+                    "residency": "dataset mirrored in HBM before timing (SharedInput.mirror, SURVEY 8(f)#1); with "
+                                 "the dataset left in pinned host memory see gather_from_host_memory"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n_step * (2 * row_bytes + 8)),
                          "traffic_unit": "bytes/launch", "peak_kind": peak_kind,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of the committed ncu --set "
+                                           "full capture of this launch size (%s), not measured in this run"
+                                           % TRAFFIC_CAPTURE,
                          "kernel": "gather_rows_kernel<32>" if row_bytes % 32 == 0 else "gather_rows_kernel<16>", "bytes_per_launch": n_step * (2 * row_bytes + 8)},
             "single_batch_us": 1e6 * hd["single_s"],
             "gather_from_host_memory": hd["host_source"],
             "gpu_launches": n_gpus * args.steps, "clocks": hd["clocks"], "setup_s": hd["setup_s"]}
     if dist is not None:
         line["processes"] = "one per GPU for the headline (torchrun); rank 0 alone for the sub-measurements"
-    line.update(sub_measurements(args, n_gpus, peak, peak_kind))
+    line.update(sub_measurements(args, n_gpus, peak, peak_kind, dry))
+    if dry:
+        line["dry_run"] = True
+        line["data"] = "synthetic timings (dry run: no GPU work)"
     return line
+
+
+def gather_cpu_baseline(args):
+    """The unmodified reference's call(indexes) (no-op kernel) on this box's
+    cores: a bounded sample (5 steps) of the headline workload."""
+    cores = os.cpu_count() or 1
+    res, err = run_reference_driver("gather", ["--rows", args.rows, "--cols", args.cols, "--batch",
+                                               args.batch * args.batches, "--steps", 5, "--warmup", 1,
+                                               "--workers", cores])
+    if not res:
+        return {"value": None, "unavailable": err}
+    return {"value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference", "cpu_model": cpu_model(),
+            "sample": "5 steps x %d rows via the unmodified reference call(indexes), no-op kernel, from the same "
+                      "%dx%d f32 dataset shape" % (args.batch * args.batches, args.rows, args.cols)}
 
 
 def main():
@@ -711,17 +959,22 @@ def main():
     rank, world, dist = dist_setup()
     n_gpus = max(args.gpus, world)
     line = None
+    seen = None
+    if args.dry_run and dist is not None:
+        seen = [None] * world
+        dist.all_gather_object(seen, {"rank": rank, "pid": os.getpid()})
     if args.dry_run:
-        # Coordination only: every rank reports in, rank 0 alone prints.
-        if dist is not None:
-            import torch
-
-            seen = [None] * world
-            dist.all_gather_object(seen, {"rank": rank, "pid": os.getpid()})
-        else:
-            seen = [{"rank": 0, "pid": os.getpid()}]
-        line = {"metric": METRIC, "dry_run": True, "n_gpus": n_gpus, "world": world,
-                "ranks_seen": sorted(s["rank"] for s in seen), "driver_rank": 0}
+        # No GPU work: every rank reports in, rank 0 assembles the full line
+        # from synthetic device timings (the CPU reference legs run for real).
+        if rank == 0:
+            if args.impl == "reference":
+                line = reference_arm(args, n_gpus)
+            else:
+                line = ours(args, n_gpus, world=world, dry=True)
+                if not args.no_cpu_baseline:
+                    line["cpu_baseline"] = gather_cpu_baseline(args)
+            line.update({"dry_run": True, "world": world, "driver_rank": 0,
+                         "ranks_seen": sorted(x["rank"] for x in seen) if seen else [0]})
     elif args.impl == "ours" and dist is not None:
         # torchrun: one process per GPU for the headline, rank 0 then drives the rest
         import paper_1710_04162_b200 as sk
@@ -734,15 +987,7 @@ def main():
         else:
             line = ours(args, n_gpus)
             if not args.no_cpu_baseline:
-                cores = os.cpu_count() or 1
-                res, err = run_reference_driver("gather", ["--rows", args.rows, "--cols", args.cols, "--batch",
-                                                           args.batch * args.batches, "--steps", 5, "--warmup", 1,
-                                                           "--workers", cores])
-                line["cpu_baseline"] = (
-                    {"value": res["gbs"], "unit": "GB/s", "cores": res["workers"], "kind": "reference",
-                     "sample": "5 steps x %d rows via the unmodified reference call(indexes), no-op kernel, from the "
-                               "same %dx%d f32 dataset shape" % (args.batch * args.batches, args.rows, args.cols)}
-                    if res else {"value": None, "unavailable": err})
+                line["cpu_baseline"] = gather_cpu_baseline(args)
     if dist is not None:
         dist.barrier()
     if rank == 0:

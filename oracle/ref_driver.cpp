@@ -141,24 +141,34 @@ static int run_sgd(int argc, char** argv) {
     SyncSgd trainer(pool, block, SgdRule{}, 0.01);
     std::mt19937_64 rng(42);
     std::uniform_int_distribution<std::size_t> pick(0, ds_rows - 1);
-    double timed = 0.0, allreduce = 0.0, loss = 0.0;
+    // Table-1 accounting of the reference's own bench (src/bench.cpp:186-198):
+    // function = grad + step compute means, shuffle = index selection +
+    // grad-call scatter, straggler = grad + step stragglers, all-reduce.
+    double timed = 0.0, allreduce = 0.0, function_s = 0.0, shuffle = 0.0, straggler = 0.0, loss = 0.0;
     for (long s = 0; s < warmup + steps; ++s) {
+        auto t0 = Clock::now();
         IndexList idx(batch);
         for (auto& i : idx) i = pick(rng);
         CallOptions o;
         o.indexes = IndexSelection(std::move(idx));
-        auto t0 = Clock::now();
+        const double select_s = std::chrono::duration<double>(Clock::now() - t0).count();
         loss = trainer.train_step(f, {FunctionArg(sx), FunctionArg(sy)}, o);
         double d = std::chrono::duration<double>(Clock::now() - t0).count();
         if (s >= warmup) {
+            const StepReport& sr = trainer.last_report();
             timed += d;
-            allreduce += trainer.last_report().allreduce_s;
+            allreduce += sr.allreduce_s;
+            function_s += sr.grad_call.compute_mean_s() + sr.step_call.compute_mean_s();
+            shuffle += select_s + sr.grad_call.scatter_s;
+            straggler += sr.grad_call.straggler_s + sr.step_call.straggler_s;
         }
     }
     std::printf("{\"mode\": \"sgd\", \"batch\": %zu, \"steps\": %ld, \"workers\": %zu, \"seconds\": %.6f,"
-                " \"ms_per_step\": %.4f, \"samples_per_s\": %.3f, \"allreduce_s_mean\": %.6f, \"loss\": %.9g}\n",
+                " \"ms_per_step\": %.4f, \"samples_per_s\": %.3f, \"allreduce_s_mean\": %.6f, \"loss\": %.9g,"
+                " \"table1\": {\"total_s\": %.6f, \"function_s\": %.6f, \"shuffle_s\": %.6f, \"straggler_s\": %.6f,"
+                " \"allreduce_s\": %.6f}}\n",
                 batch, steps, workers, timed, 1e3 * timed / steps, double(batch) * steps / timed, allreduce / steps,
-                loss);
+                loss, timed, function_s, shuffle, straggler, allreduce);
     return 0;
 }
 

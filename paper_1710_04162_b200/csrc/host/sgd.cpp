@@ -2,6 +2,7 @@
 
 #include "synkpar/sgd.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 
@@ -200,13 +201,20 @@ const StepReport& SyncSgd::last_report() const {
     if (report_pending_ && timers_) {
         report_pending_ = false;
         const auto& t = timers_->per_rank;
-        double scatter = 0.0, sec = 0.0;
+        double scatter = 0.0, sec = 0.0, task_max = 0.0, task_sum = 0.0;
         last_.grad_call.rank_compute_s.assign(t.size(), 0.0);
         for (std::size_t r = 0; r < t.size(); ++r) {
             if (synk_timer_elapsed(t[r], 0, 1, &sec) == SYNK_OK) scatter += sec;
             if (synk_timer_elapsed(t[r], 1, 3, &sec) == SYNK_OK) last_.grad_call.rank_compute_s[r] = sec;
+            // rank task = its share on the device, staging through compute end
+            if (synk_timer_elapsed(t[r], 0, 3, &sec) == SYNK_OK) {
+                task_max = std::max(task_max, sec);
+                task_sum += sec;
+            }
         }
         last_.grad_call.scatter_s = scatter / double(t.size());
+        // straggler = max - mean rank task (function.hpp CallReport)
+        if (!t.empty()) last_.grad_call.straggler_s = task_max - task_sum / double(t.size());
         if (!t.empty() && synk_timer_elapsed(t[0], update_from_compute_end_ ? 3 : 4, 5, &sec) == SYNK_OK) {
             last_.allreduce_s = sec;
             last_.step_call.total_s = sec;
