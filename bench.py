@@ -818,7 +818,9 @@ def sync_sgd_section(sk, args, n_gpus, model, dry=False):
            "table1_note": "function = gradient-call compute (mean over ranks, device events); shuffle = staging of "
                           "the indexed batch before compute (0 when the gather is fused into the compute graph); "
                           "straggler = max - mean rank task; allreduce = the fused all-reduce + 1/W + update "
-                          "kernel (so the update sits here, not in function)"}
+                          "kernel (so the update sits here, not in function); for C5 the all-reduce + update runs "
+                          "per layer on a second stream, overlapped with the backward GEMMs, so its span overlaps "
+                          "function and the parts sum to more than total"}
     if model == "c5":
         bf16_peak, bf16_sustained, peak_kind = 1609.7, 1365.0, "fallback"
         try:

@@ -29,6 +29,7 @@
 #include <thread>
 #include <vector>
 
+#include "synkpar/bench.hpp"
 #include "synkpar/function.hpp"
 #include "synkpar/mlp.hpp"
 #include "synkpar/sgd.hpp"
@@ -172,6 +173,39 @@ static int run_sgd(int argc, char** argv) {
     return 0;
 }
 
+// The reference's own trainer benchmark (src/bench.cpp run_bench): the loss
+// of every step of every run, for trajectory comparisons with ours.
+static int run_bench_mode(int argc, char** argv) {
+    BenchConfig c;
+    c.workers.clear();
+    const std::string w = sarg(argc, argv, "--workers-list", "1,2");
+    for (std::size_t at = 0; at < w.size();) {
+        std::size_t comma = w.find(',', at);
+        if (comma == std::string::npos) comma = w.size();
+        c.workers.push_back(std::stoul(w.substr(at, comma - at)));
+        at = comma + 1;
+    }
+    c.steps = arg(argc, argv, "--steps", 4);
+    c.batch = arg(argc, argv, "--batch", 16);
+    c.batch_mode = sarg(argc, argv, "--batch-mode", "scaled") == "fixed" ? BatchMode::Fixed : BatchMode::ScaledByWorkers;
+    c.width = arg(argc, argv, "--width", 32);
+    c.layers = arg(argc, argv, "--layers", 2);
+    c.seed = arg(argc, argv, "--seed", 0);
+    c.in_dim = arg(argc, argv, "--in", 16);
+    c.out_dim = arg(argc, argv, "--out", 4);
+    c.pin_threads = false;
+    BenchReport rep = run_bench(c);
+    std::printf("{\"mode\": \"bench\", \"runs\": [");
+    for (std::size_t i = 0; i < rep.runs.size(); ++i) {
+        std::printf("%s{\"workers\": %zu, \"losses\": [", i ? ", " : "", rep.runs[i].workers);
+        for (std::size_t k = 0; k < rep.runs[i].losses.size(); ++k)
+            std::printf("%s%.17g", k ? ", " : "", rep.runs[i].losses[k]);
+        std::printf("]}");
+    }
+    std::printf("]}\n");
+    return 0;
+}
+
 static int run_slicing(int argc, char** argv) {
     const std::size_t rows = arg(argc, argv, "--rows", 262144), cols = arg(argc, argv, "--cols", 1024);
     const std::size_t slices = arg(argc, argv, "--slices", 4);
@@ -267,6 +301,7 @@ int main(int argc, char** argv) {
         if (mode == "gather") return run_gather(argc, argv);
         if (mode == "sgd") return run_sgd(argc, argv);
         if (mode == "slicing") return run_slicing(argc, argv);
+        if (mode == "bench") return run_bench_mode(argc, argv);
         if (mode == "collective") return run_collective(argc, argv);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "ref_driver: %s\n", e.what());
