@@ -287,6 +287,40 @@ int synk_gemm_tc(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, co
  * The tensor cores read MN-major shared-memory tiles directly (UMMA major
  * bits), so the MLP's weight/activation/delta transposes (mlp.cpp:31-73,
  * 169-208 use W^T, a^T, delta^T) are never materialised. */
+/* bf16 weight shadow: a per-rank HBM copy of an MLP's weight matrices in the
+ * bf16 operand layout of the tensor-core path (W_l row-major with padded
+ * leading dimension, plus W_l^T for narrow layers). The fused update writes
+ * it together with the new f32 params, so the next step's products read it
+ * directly instead of re-casting 100 MB of f32 weights (replaces the per-step
+ * cast of mlp.cpp's f64 widening on the bf16 path). Layout per rank:
+ * synk_mlp_bf16_shadow(). off_wt == SYNK_NO_TRANSPOSE: no transposed copy. */
+#define SYNK_SHADOW_MAX_SEGS 8
+#define SYNK_SHADOW_MAX_WORLD 8
+#define SYNK_NO_TRANSPOSE (~(uint64_t)0)
+typedef struct synk_bf16_shadow_seg {
+    uint64_t first;       /* element offset of W_l in the flat parameter block */
+    uint64_t rows, cols;  /* d_l x d_{l+1} */
+    uint64_t off_w, ldw;  /* byte offset of bf16 W_l in the shadow, leading dim (elements) */
+    uint64_t off_wt, ldwt;/* byte offset of bf16 W_l^T, leading dim; or SYNK_NO_TRANSPOSE */
+} synk_bf16_shadow_seg;
+typedef struct synk_bf16_shadow {
+    uint32_t count;       /* weight segments */
+    uint64_t bytes;       /* shadow buffer size per rank */
+    synk_bf16_shadow_seg seg[SYNK_SHADOW_MAX_SEGS];
+} synk_bf16_shadow;
+int synk_mlp_bf16_shadow(const uint64_t* dims, uint32_t layers, synk_bf16_shadow* out);
+
+/* synk_all_reduce_step over the flat range [elem_base, elem_base + n) of a
+ * larger block (the pointers are already offset by elem_base), additionally
+ * writing bf16(new params) into every rank's shadow (shadow_bases[q], layout
+ * `shadow`) for the elements that fall in a shadow weight segment. shadow may
+ * be NULL (plain synk_all_reduce_step). f32 only, world <= SYNK_SHADOW_MAX_WORLD. */
+int synk_all_reduce_step_ex(synk_dev* dev, int world, int dtype, int grad_op, int rule,
+                            const double* hyper, double lr, uint64_t t, void* const* params,
+                            void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
+                            int replicas_coherent, uint64_t elem_base, const synk_bf16_shadow* shadow,
+                            void* const* shadow_bases);
+
 #define SYNK_GEMM_A_MN 1
 #define SYNK_GEMM_B_MN 2
 int synk_gemm_tc2(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, const void* a_hi, const void* a_lo,
@@ -316,6 +350,32 @@ int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t
                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
                            void* grad, void* workspace, uint64_t workspace_bytes, int signal_base,
                            int* signalled, const uint64_t* rows);
+/* Options of synk_mlp_loss_grad_opts (all optional; zero-initialise).
+ *   signal_base      as synk_mlp_loss_grad_seg (-1: no segment signals)
+ *   rows             index-fused batch rows in HBM (as synk_mlp_loss_grad_seg)
+ *   rows_host        the same list as a device-readable alias of page-locked
+ *                    host memory, or NULL: the bf16 x staging may read it in
+ *                    place instead of waiting for `rows` to be filled
+ *   rows_ready_on / rows_ready_slot: `rows` is filled once the slot event of
+ *                    that handle fires (synk_signal_slot); the stream waits on
+ *                    it before the first read of `rows`. NULL: ready now.
+ *   shadow           bf16 weight shadow (synk_mlp_bf16_shadow layout) of this
+ *                    rank, bf16 path only; NULL: casts into the workspace
+ *   shadow_valid     1: the shadow equals bf16(params): the casts are skipped;
+ *                    0: the casts write the shadow (valid afterwards). */
+typedef struct synk_mlp_opts {
+    int signal_base;
+    const uint64_t* rows;
+    const uint64_t* rows_host;
+    synk_dev* rows_ready_on;
+    int rows_ready_slot;
+    void* shadow;
+    int shadow_valid;
+} synk_mlp_opts;
+int synk_mlp_loss_grad_opts(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
+                            void* grad, void* workspace, uint64_t workspace_bytes, const synk_mlp_opts* opts,
+                            int* signalled);
 /* Same with a compute mode: SYNK_MLP_NATIVE runs every product in the
  * parameter dtype on the CUDA cores (f32 FFMA / f64 DFMA); SYNK_MLP_BF16_TC
  * (f32 parameters only) runs every dense product on tcgen05 tensor cores

@@ -93,6 +93,14 @@ struct KernelContext {
     struct IndexedInput {
         const std::uint64_t* rows = nullptr;
         std::size_t count = 0;
+        // The same list readable in place by kernels when the caller's list
+        // is page-locked (device alias of host memory), else nullptr.
+        const std::uint64_t* host_rows = nullptr;
+        // rows is being filled on the rank's copy stream: a consumer's stream
+        // waits on slot `ready_slot` of `ready_on` (synk_wait_peer_slot)
+        // before its first read of rows. nullptr: filled already.
+        synk_dev* ready_on = nullptr;
+        int ready_slot = -1;
     };
     const std::vector<IndexedInput>* indexed = nullptr;
 };

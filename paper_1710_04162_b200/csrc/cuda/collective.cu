@@ -16,7 +16,9 @@
 // 2(W-1)/W x bytes, the same as a ring all-reduce, in a single kernel with no
 // intermediate synchronisation (chunks are disjoint, so ranks never race).
 
+#include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "optim_math.cuh"
@@ -158,67 +160,167 @@ __global__ void __launch_bounds__(kBlock) bcast_chunk_kernel(Ptrs bufs, int w, i
 }
 
 // ---- fused gradient all-reduce + optimizer update ------------------------------
-// Vector body: one 16-byte vector (4 f32 / 2 f64 elements) of chunk r per
-// iteration: W peer loads of the gradient, per-lane tree fold + 1/W, then the
-// update on this rank's (coherent) params/aux and W peer stores of each.
-// With W == 1 the fold is the identity (and x*1.0 is exact), so the gradient
-// is not rewritten.
-template <class T, int W>
+// Vector body: one 32-byte vector (8 f32 / 4 f64 elements; sm_100
+// ld/st.global.v8.b32, 16-byte lanes when a pointer is not 32-byte aligned)
+// of chunk r per iteration: W peer loads of the gradient, per-lane tree fold
+// + 1/W, then the update on this rank's (coherent) params/aux and W peer
+// stores of each. With W == 1 the fold is the identity (and x*1.0 is exact),
+// so the gradient is not rewritten.
+
+template <class T, int BYTES>
+struct VecT {
+    static constexpr int N = BYTES / (int)sizeof(T);
+    T e[N];
+};
+
+template <class T, int BYTES>
+__device__ __forceinline__ VecT<T, BYTES> vload(const void* base, uint64_t v) {
+    VecT<T, BYTES> x;
+    const char* p = static_cast<const char*>(base) + v * BYTES;
+    if constexpr (BYTES == 32) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+        asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                     : "l"(p));
+    } else {
+        *reinterpret_cast<uint4*>(&x) = *reinterpret_cast<const uint4*>(p);
+    }
+    return x;
+}
+
+template <class T, int BYTES>
+__device__ __forceinline__ void vstore(void* base, uint64_t v, const VecT<T, BYTES>& x) {
+    char* p = static_cast<char*>(base) + v * BYTES;
+    if constexpr (BYTES == 32) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                     "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+    } else {
+        *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(&x);
+    }
+}
+
+// bf16 weight shadow written along with the new params (synk_cuda.h).
+struct Shadow {
+    void* base[SYNK_SHADOW_MAX_WORLD];
+    uint32_t count;
+    uint64_t elem_base;  // flat index of the kernel's element 0
+    synk_bf16_shadow_seg seg[SYNK_SHADOW_MAX_SEGS];
+};
+
+__device__ __forceinline__ int shadow_find(const Shadow& sh, uint64_t gi) {
+    for (uint32_t s = 0; s < sh.count; ++s)
+        if (gi >= sh.seg[s].first && gi - sh.seg[s].first < sh.seg[s].rows * sh.seg[s].cols) return (int)s;
+    return -1;
+}
+
+// Elements [gi, gi + N) of the flat block, new f32 values v: their bf16
+// copies into replica q's shadow (same rounding as the cast kernels).
+template <int N>
+__device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t gi, const float* v) {
+    int s = shadow_find(sh, gi);
+    if (s < 0 && N > 1) s = shadow_find(sh, gi + N - 1);  // a segment may start inside the vector
+    if (s < 0) return;
+    const synk_bf16_shadow_seg& g = sh.seg[s];
+    char* b = static_cast<char*>(sh.base[q]);
+    __nv_bfloat16* w = reinterpret_cast<__nv_bfloat16*>(b + g.off_w);
+    __nv_bfloat16* wt = g.off_wt == SYNK_NO_TRANSPOSE ? nullptr : reinterpret_cast<__nv_bfloat16*>(b + g.off_wt);
+    const uint64_t size = g.rows * g.cols;
+    if (N == 8 && gi >= g.first && gi + 8 <= g.first + size) {
+        const uint64_t o = gi - g.first, r = o / g.cols, c = o - r * g.cols;
+        const uint64_t at = r * g.ldw + c;
+        if (c + 8 <= g.cols && (at & 7) == 0) {  // one row, 16-byte aligned: one store
+            __nv_bfloat162 h[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            *reinterpret_cast<uint4*>(w + at) = *reinterpret_cast<const uint4*>(h);
+            if (wt)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) wt[(c + k) * g.ldwt + r] = __float2bfloat16_rn(v[k]);
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const uint64_t e = gi + k;
+        int sk = shadow_find(sh, e);
+        if (sk < 0) continue;
+        const synk_bf16_shadow_seg& gk = sh.seg[sk];
+        __nv_bfloat16* wk = reinterpret_cast<__nv_bfloat16*>(b + gk.off_w);
+        const uint64_t o = e - gk.first, r = o / gk.cols, c = o - r * gk.cols;
+        const __nv_bfloat16 h = __float2bfloat16_rn(v[k]);
+        wk[r * gk.ldw + c] = h;
+        if (gk.off_wt != SYNK_NO_TRANSPOSE) reinterpret_cast<__nv_bfloat16*>(b + gk.off_wt)[c * gk.ldwt + r] = h;
+    }
+}
+
+template <class T, int W, int BYTES, bool SH>
 __device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
                                             int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
-                                            int naux, uint64_t v) {
-    using V = typename V16<T>::V;
-    constexpr int N = V16<T>::N;
+                                            int naux, uint64_t v, const Shadow& sh) {
+    using V = VecT<T, BYTES>;
+    constexpr int N = V::N;
     V gx[W];
 #pragma unroll
-    for (int q = 0; q < W; ++q) gx[q] = static_cast<const V*>(grads.p[q])[v];
+    for (int q = 0; q < W; ++q) gx[q] = vload<T, BYTES>(grads.p[q], v);
     V g;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         T e[W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) e[q] = reinterpret_cast<const T*>(&gx[q])[k];
-        reinterpret_cast<T*>(&g)[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
+        for (int q = 0; q < W; ++q) e[q] = gx[q].e[k];
+        g.e[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
     }
     if constexpr (W > 1) {
 #pragma unroll
-        for (int q = 0; q < W; ++q) static_cast<V*>(grads.p[q])[v] = g;
+        for (int q = 0; q < W; ++q) vstore<T, BYTES>(grads.p[q], v, g);
     }
-    V p = static_cast<const V*>(params.p[rank])[v];
-    V a0 = naux > 0 ? static_cast<const V*>(aux0.p[rank])[v] : p;
-    V a1 = naux > 1 ? static_cast<const V*>(aux1.p[rank])[v] : p;
+    V p = vload<T, BYTES>(params.p[rank], v);
+    V a0 = naux > 0 ? vload<T, BYTES>(aux0.p[rank], v) : p;
+    V a1 = naux > 1 ? vload<T, BYTES>(aux1.p[rank], v) : p;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-        double pd = (double)reinterpret_cast<T*>(&p)[k];
-        double x0 = (double)reinterpret_cast<T*>(&a0)[k];
-        double x1 = (double)reinterpret_cast<T*>(&a1)[k];
-        synk::rule_update(rp, pd, x0, x1, (double)reinterpret_cast<T*>(&g)[k]);
-        reinterpret_cast<T*>(&p)[k] = (T)pd;
-        reinterpret_cast<T*>(&a0)[k] = (T)x0;
-        reinterpret_cast<T*>(&a1)[k] = (T)x1;
+        double pd = (double)p.e[k];
+        double x0 = (double)a0.e[k];
+        double x1 = (double)a1.e[k];
+        synk::rule_update(rp, pd, x0, x1, (double)g.e[k]);
+        p.e[k] = (T)pd;
+        a0.e[k] = (T)x0;
+        a1.e[k] = (T)x1;
     }
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-        static_cast<V*>(params.p[q])[v] = p;
-        if (naux > 0) static_cast<V*>(aux0.p[q])[v] = a0;
-        if (naux > 1) static_cast<V*>(aux1.p[q])[v] = a1;
+        vstore<T, BYTES>(params.p[q], v, p);
+        if (naux > 0) vstore<T, BYTES>(aux0.p[q], v, a0);
+        if (naux > 1) vstore<T, BYTES>(aux1.p[q], v, a1);
+        if constexpr (SH) shadow_store<N>(sh, q, sh.elem_base + v * N, reinterpret_cast<const float*>(p.e));
     }
 }
 
-template <class T, int W>
+template <class T, int W, bool SH>
 __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
-    double inv_w, synk::RuleParams rp, int naux, bool coherent, uint64_t lo, uint64_t hi, bool vec) {
+    double inv_w, synk::RuleParams rp, int naux, bool coherent, uint64_t lo, uint64_t hi, int vec_bytes, Shadow sh) {
     const int fop = grad_op == SYNK_OP_MEAN ? SYNK_OP_SUM : grad_op;
     uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     uint64_t stride = (uint64_t)gridDim.x * kBlock;
     if constexpr (W > 0) {
-        if (vec && coherent) {
-            constexpr int N = V16<T>::N;
-            const uint64_t v0 = lo / N, v1 = hi / N;  // lo is 16-element aligned
-            for (uint64_t v = v0 + tid; v < v1; v += stride)
-                step_vector<T, W>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v);
-            lo = v1 * N;  // scalar tail below
+        if (vec_bytes && coherent) {
+            // lo is 16-element aligned, so a multiple of both vector widths
+            if (vec_bytes == 32) {
+                constexpr int N = VecT<T, 32>::N;
+                const uint64_t v0 = lo / N, v1 = hi / N;
+                for (uint64_t v = v0 + tid; v < v1; v += stride)
+                    step_vector<T, W, 32, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh);
+                lo = v1 * N;  // scalar tail below
+            } else {
+                constexpr int N = VecT<T, 16>::N;
+                const uint64_t v0 = lo / N, v1 = hi / N;
+                for (uint64_t v = v0 + tid; v < v1; v += stride)
+                    step_vector<T, W, 16, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh);
+                lo = v1 * N;
+            }
         }
     }
     for (uint64_t i = lo + tid; i < hi; i += stride) {
@@ -246,6 +348,10 @@ __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
                 static_cast<T*>(params.p[q])[i] = pt;
                 if (naux > 0) static_cast<T*>(aux0.p[q])[i] = a0t;
                 if (naux > 1) static_cast<T*>(aux1.p[q])[i] = a1t;
+                if constexpr (SH) {
+                    const float f = (float)pt;
+                    shadow_store<1>(sh, q, sh.elem_base + i, &f);
+                }
             }
         } else {
             for (int q = 0; q < world; ++q) {
@@ -256,6 +362,10 @@ __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
                 static_cast<T*>(params.p[q])[i] = (T)p;
                 if (naux > 0) static_cast<T*>(aux0.p[q])[i] = (T)a0;
                 if (naux > 1) static_cast<T*>(aux1.p[q])[i] = (T)a1;
+                if constexpr (SH) {
+                    const float f = (float)(T)p;
+                    shadow_store<1>(sh, q, sh.elem_base + i, &f);
+                }
             }
         }
     }
@@ -327,10 +437,16 @@ int allreduce_t(synk_dev* d, int w, int op, void* const* bufs, uint64_t n, bool 
     return SYNK_OK;
 }
 
+bool ptrs_aligned(void* const* bufs, int w, uintptr_t align) {
+    uintptr_t acc = 0;
+    for (int q = 0; q < w; ++q) acc |= (uintptr_t)bufs[q];
+    return (acc & (align - 1)) == 0;
+}
+
 template <class T>
 int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp, void* const* params,
                      void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
-                     bool coherent) {
+                     bool coherent, const Shadow* sh) {
     Ptrs P{}, G{}, A0{}, A1{};
     int naux = synk::rule_aux_count(rp.rule);
     if (int rc = fill_ptrs(&P, params, w); rc != SYNK_OK) return rc;
@@ -347,21 +463,39 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     chunk_of(n, w, d->rank, &lo, &hi);
     if (lo >= hi) return SYNK_OK;
     double inv_w = 1.0 / (double)w;
-    bool vec = ptrs_aligned16(params, w) && ptrs_aligned16(grads, w) && (naux < 1 || ptrs_aligned16(aux0, w)) &&
-               (naux < 2 || ptrs_aligned16(aux1, w));
-    unsigned grid = synk::grid_for(d, vec ? (hi - lo) / V16<T>::N + 1 : hi - lo, kBlock);
+    auto aligned = [&](uintptr_t a) {
+        return ptrs_aligned(params, w, a) && ptrs_aligned(grads, w, a) && (naux < 1 || ptrs_aligned(aux0, w, a)) &&
+               (naux < 2 || ptrs_aligned(aux1, w, a));
+    };
+    // 256-bit lanes when every pointer allows them (the measured winner on the
+    // gather, profiles/r01_gather.md), else 16-byte lanes, else scalar.
+    static const int forced = [] {
+        const char* e = getenv("SYNK_UPDATE_VEC");  // A/B: 16 forces 16-byte lanes
+        return e ? atoi(e) : 0;
+    }();
+    const int vec_bytes = aligned(32) && forced != 16 ? 32 : (aligned(16) ? 16 : 0);
+    const uint64_t items = vec_bytes ? (hi - lo) / (vec_bytes / sizeof(T)) + 1 : hi - lo;
+    unsigned grid = synk::grid_for(d, items, kBlock);
+    Shadow none{};
+    const Shadow& S = sh ? *sh : none;
+    const bool with = sh != nullptr;
     switch (w) {
-#define SYNK_ARS_CASE(WW)                                                                        \
-    case WW:                                                                                     \
-        allreduce_step_kernel<T, WW><<<grid, kBlock, 0, d->stream>>>(                            \
-            P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec);          \
+#define SYNK_ARS_CASE(WW)                                                                                        \
+    case WW:                                                                                                     \
+        if (with)                                                                                                \
+            allreduce_step_kernel<T, WW, true><<<grid, kBlock, 0, d->stream>>>(                                  \
+                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec_bytes, S);             \
+        else                                                                                                     \
+            allreduce_step_kernel<T, WW, false><<<grid, kBlock, 0, d->stream>>>(                                 \
+                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec_bytes, S);             \
         break;
         SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(3) SYNK_ARS_CASE(4)
         SYNK_ARS_CASE(5) SYNK_ARS_CASE(6) SYNK_ARS_CASE(7) SYNK_ARS_CASE(8)
 #undef SYNK_ARS_CASE
     default:
-        allreduce_step_kernel<T, 0><<<grid, kBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
-                                                                    inv_w, rp, naux, coherent, lo, hi, false);
+        SYNK_REQUIRE(!with, SYNK_EARG, "all_reduce_step: bf16 shadows need world <= 8");
+        allreduce_step_kernel<T, 0, false><<<grid, kBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
+                                                                           inv_w, rp, naux, coherent, lo, hi, 0, S);
     }
     SYNK_LAUNCHED("allreduce_step_kernel");
     return SYNK_OK;
@@ -495,8 +629,35 @@ int synk_all_reduce_step(synk_dev* d, int world, int dtype, int grad_op, int rul
     if (n == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     return dtype == SYNK_F32
-               ? allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent)
-               : allreduce_step_t<double>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent);
+               ? allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, nullptr)
+               : allreduce_step_t<double>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, nullptr);
+}
+
+int synk_all_reduce_step_ex(synk_dev* d, int world, int dtype, int grad_op, int rule, const double* hyper,
+                            double lr, uint64_t t, void* const* params, void* const* grads,
+                            void* const* aux0, void* const* aux1, uint64_t n, int coherent, uint64_t elem_base,
+                            const synk_bf16_shadow* shadow, void* const* shadow_bases) {
+    if (!shadow)
+        return synk_all_reduce_step(d, world, dtype, grad_op, rule, hyper, lr, t, params, grads, aux0, aux1, n,
+                                    coherent);
+    SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EDTYPE, "all_reduce_step: bf16 shadows need f32 params");
+    SYNK_REQUIRE(world >= 1 && world <= SYNK_SHADOW_MAX_WORLD, SYNK_EARG, "all_reduce_step: shadows need world <= 8");
+    SYNK_REQUIRE(shadow->count <= SYNK_SHADOW_MAX_SEGS && shadow_bases, SYNK_EARG, "all_reduce_step: bad shadow");
+    SYNK_REQUIRE(grad_op >= SYNK_OP_SUM && grad_op <= SYNK_OP_PROD, SYNK_EARG,
+                 "all_reduce: Gather is not a reduction (use gather())");
+    synk::RuleParams rp;
+    if (int rc = make_rule(rule, hyper, lr, t, &rp); rc != SYNK_OK) return rc;
+    if (n == 0) return SYNK_OK;
+    Shadow S{};
+    for (int q = 0; q < world; ++q) {
+        SYNK_REQUIRE(shadow_bases[q], SYNK_EARG, "all_reduce_step: missing shadow");
+        S.base[q] = shadow_bases[q];
+    }
+    S.count = shadow->count;
+    S.elem_base = elem_base;
+    for (uint32_t k = 0; k < shadow->count; ++k) S.seg[k] = shadow->seg[k];
+    synk::DeviceGuard g(d->device);
+    return allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, &S);
 }
 
 }  // extern "C"

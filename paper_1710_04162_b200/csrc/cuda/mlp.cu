@@ -426,25 +426,77 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
     return p;
 }
 
+// bf16 weight shadow layout (synk_cuda.h): W_l with leading dim pad8(d_{l+1})
+// and, for narrow layers, W_l^T with leading dim pad8(d_l) -- exactly the
+// operand buffers the products read.
+int bf16_shadow_layout(const uint64_t* dims, uint32_t L, const Plan& P, synk_bf16_shadow* out) {
+    SYNK_REQUIRE(L <= SYNK_SHADOW_MAX_SEGS, SYNK_EARG, "mlp: bf16 shadow supports up to 8 layers");
+    *out = synk_bf16_shadow{};
+    uint64_t at = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t o = at;
+        at += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    out->count = L;
+    for (uint32_t l = 0; l < L; ++l) {
+        synk_bf16_shadow_seg& g = out->seg[l];
+        g.first = P.woff[l];
+        g.rows = dims[l];
+        g.cols = dims[l + 1];
+        g.ldw = pad8(dims[l + 1]);
+        g.off_w = take(dims[l] * g.ldw * 2);
+        g.ldwt = pad8(dims[l]);
+        g.off_wt = dims[l + 1] <= kWideN ? take(dims[l + 1] * g.ldwt * 2) : SYNK_NO_TRANSPOSE;
+    }
+    out->bytes = at;
+    return SYNK_OK;
+}
+
 int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P, const float* theta, const float* x,
                    const float* y, uint64_t n, double* loss, float* grad, void* ws, int signal_base = -1,
-                   const uint64_t* rows = nullptr) {
+                   const uint64_t* rows = nullptr, const synk_mlp_opts* opts = nullptr) {
     Bf16Plan B = make_bf16_plan(dims, L, n, P.maxd);
     char* base = static_cast<char*>(ws);
     auto bf = [&](uint64_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
     const int F32 = SYNK_F32, BF = SYNK_BF16;
     auto wide = [&](uint32_t l) { return dims[l + 1] > kWideN; };  // output width of layer l
 
-    // weights: W_l in bf16 (+ W_l^T for narrow layers), one read each
-    for (uint32_t l = 0; l < L; ++l) {
-        const float* W = theta + P.woff[l];
-        if (int rc = synk_gemm_prep2_bf16(d, W, dims[l], dims[l + 1], dims[l + 1], bf(B.off_w[l]), pad8(dims[l + 1]),
-                                          wide(l) ? nullptr : bf(B.off_wt[l]), pad8(dims[l]));
-            rc)
-            return rc;
+    // weights: W_l in bf16 (+ W_l^T for narrow layers), one read each -- into
+    // the rank's persistent shadow when given (skipped when it is current:
+    // the fused update of the previous step wrote it with the new params)
+    synk_bf16_shadow sh{};
+    char* shb = opts && opts->shadow ? static_cast<char*>(opts->shadow) : nullptr;
+    if (shb)
+        if (int rc = bf16_shadow_layout(dims, L, P, &sh); rc) return rc;
+    auto wbuf = [&](uint32_t l) { return shb ? reinterpret_cast<__nv_bfloat16*>(shb + sh.seg[l].off_w) : bf(B.off_w[l]); };
+    auto wtbuf = [&](uint32_t l) {
+        return shb ? reinterpret_cast<__nv_bfloat16*>(shb + sh.seg[l].off_wt) : bf(B.off_wt[l]);
+    };
+    if (!shb || !opts->shadow_valid)
+        for (uint32_t l = 0; l < L; ++l) {
+            const float* W = theta + P.woff[l];
+            if (int rc = synk_gemm_prep2_bf16(d, W, dims[l], dims[l + 1], dims[l + 1], wbuf(l), pad8(dims[l + 1]),
+                                              wide(l) ? nullptr : wtbuf(l), pad8(dims[l]));
+                rc)
+                return rc;
+        }
+    // index-fused rows: staged into HBM by the executor (possibly still in
+    // flight on its copy stream), and/or readable in place in pinned host memory
+    bool rows_waited = !(opts && opts->rows_ready_on);
+    auto wait_rows = [&]() -> int {
+        if (rows_waited) return SYNK_OK;
+        rows_waited = true;
+        return synk_wait_peer_slot(d, opts->rows_ready_on, opts->rows_ready_slot);
+    };
+    const uint64_t* xrows = rows;
+    if (rows && opts && opts->rows_host) {
+        xrows = opts->rows_host;  // the x staging reads the list over PCIe, no wait for the stage copy
+    } else if (rows) {
+        if (int rc = wait_rows(); rc) return rc;
     }
     // input batch: x and x^T in bf16 (rows != null: gathered from the whole source in the same pass)
-    if (int rc = synk_gemm_prep2_bf16_rows(d, x, rows, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]),
+    if (int rc = synk_gemm_prep2_bf16_rows(d, x, xrows, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]),
                                            bf(B.off_actT[0]), pad8(n));
         rc)
         return rc;
@@ -460,7 +512,7 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     float* pred = reinterpret_cast<float*>(base + B.off_pred);
     for (uint32_t l = 0; l < L; ++l) {
         const bool hidden = l + 1 < L;
-        const void* b = wide(l) ? (const void*)bf(B.off_w[l]) : (const void*)bf(B.off_wt[l]);
+        const void* b = wide(l) ? (const void*)wbuf(l) : (const void*)wtbuf(l);
         const uint64_t ldb = wide(l) ? pad8(dims[l + 1]) : pad8(dims[l]);
         int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, dims[l + 1], dims[l], bf(B.off_act[l]), nullptr, pad8(dims[l]), b,
                                nullptr, ldb, wide(l) ? SYNK_GEMM_B_MN : 0, hidden ? SYNK_EPI_BIAS_TANH : SYNK_EPI_BIAS,
@@ -476,6 +528,8 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
     double* partial = reinterpret_cast<double*>(base + B.off_partial);
     int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
     const double inv_n = 1.0 / (double)n;
+    if (rows)
+        if (int rc = wait_rows(); rc) return rc;  // the loss reads y through the staged list
     loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial,
                                                                  reinterpret_cast<unsigned*>(d->flags_dev + 3),
                                                                  0.5 * inv_n, loss, rows, dl);
@@ -498,20 +552,24 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
             return rc;
         // Segment [W_l, b_l] of the gradient is final, and the f32 W_l/b_l are
         // not read again in this pass (the GEMMs read the bf16 copies made at
-        // the start): the trainer may all-reduce + update it from here on.
-        if (signal_base >= 0)
+        // the start): the trainer may all-reduce + update it from here on --
+        // unless the bf16 copy is the rank's shadow, which that update
+        // rewrites: then only after dX_l below has read W_l.
+        if (signal_base >= 0 && (!shb || l == 0))
             if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
         if (l > 0) {
             // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
             const int nxt = cur ^ 1;
             const bool narrow_prev = !wide(l - 1);  // gW_{l-1} then wants delta_prev^T
             if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, din, dout, bf(B.off_d[cur]), nullptr, pad8(P.maxd),
-                                       bf(B.off_w[l]), nullptr, pad8(dout), 0, SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
+                                       wbuf(l), nullptr, pad8(dout), 0, SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
                                        pad8(P.maxd), narrow_prev ? (void*)bf(B.off_dT) : nullptr, pad8(n), nullptr,
                                        bf(B.off_act[l]), pad8(din));
                 rc)
                 return rc;
             cur = nxt;
+            if (signal_base >= 0 && shb)
+                if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
         }
     }
     return SYNK_OK;
@@ -675,6 +733,42 @@ int synk_mlp_loss_grad_seg(synk_dev* d, int dtype, int compute, const uint64_t* 
     const int rc = loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n,
                                   loss_dev, (float*)grad, workspace, signal_base, rows);
     if (rc == SYNK_OK && signal_base >= 0) *signalled = (int)layers;
+    return rc;
+}
+
+int synk_mlp_bf16_shadow(const uint64_t* dims, uint32_t layers, synk_bf16_shadow* out) {
+    Plan p;
+    if (int rc = make_plan(dims, layers, 1, &p); rc != SYNK_OK) return rc;
+    return bf16_shadow_layout(dims, layers, p, out);
+}
+
+int synk_mlp_loss_grad_opts(synk_dev* d, int dtype, int compute, const uint64_t* dims, uint32_t layers,
+                            const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,
+                            void* grad, void* workspace, uint64_t workspace_bytes, const synk_mlp_opts* opts,
+                            int* signalled) {
+    *signalled = 0;
+    synk_mlp_opts none{};
+    none.signal_base = -1;
+    const synk_mlp_opts& o = opts ? *opts : none;
+    if (compute != SYNK_MLP_BF16_TC) {
+        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE, SYNK_EARG, "mlp: unknown compute mode");
+        if (o.rows && o.rows_ready_on)  // the whole native sequence is one graph: wait up front
+            if (int rc = synk_wait_peer_slot(d, o.rows_ready_on, o.rows_ready_slot); rc) return rc;
+        return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
+                                o.rows);
+    }
+    SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
+    SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
+    SYNK_REQUIRE(o.signal_base < 0 || o.signal_base + (int)layers <= 64, SYNK_EARG,
+                 "mlp_loss_grad_seg: signal slots out of range");
+    Plan p;
+    if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
+    SYNK_REQUIRE(workspace_bytes >= make_bf16_plan(dims, layers, n, p.maxd).total, SYNK_EARG,
+                 "mlp: workspace too small");
+    synk::DeviceGuard g(d->device);
+    const int rc = loss_grad_bf16(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n,
+                                  loss_dev, (float*)grad, workspace, o.signal_base, o.rows, &o);
+    if (rc == SYNK_OK && o.signal_base >= 0) *signalled = (int)layers;
     return rc;
 }
 

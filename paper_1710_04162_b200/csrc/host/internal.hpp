@@ -94,6 +94,23 @@ struct VarRecord {
     // broadcast / all_reduce / the fused trainer step, cleared by any
     // per-rank mutation). Lets the fused step compute each chunk once.
     bool coherent = true;
+    // Bumped by every mutation of any replica (set/broadcast/reductions,
+    // scatter, function updates, trainer steps): derived copies tagged with
+    // the epoch they were made at are current iff the tag still matches.
+    std::atomic<std::uint64_t> epoch{0};
+    // Per rank: bf16 copy of an MLP's weights in the tensor-core operand
+    // layout (synk_mlp_bf16_shadow), made by the bf16 MLP kernel and kept
+    // current by the trainer's fused update. Slot r is touched only by rank
+    // r's thread (or the master between phases).
+    struct Bf16Shadow {
+        DevBuffer buf;
+        std::uint64_t epoch = ~std::uint64_t(0);  // VarRecord::epoch it matches
+        const void* params = nullptr;             // the replica storage it mirrors
+        std::vector<std::uint64_t> dims;
+        synk_bf16_shadow layout{};
+    };
+    std::vector<Bf16Shadow> shadows;
+    void mutated() { epoch.fetch_add(1); }
 };
 
 enum class PoolLifecycle : int { Idle = 0, InPhase = 1, ShutDown = 2 };

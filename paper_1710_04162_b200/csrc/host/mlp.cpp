@@ -5,6 +5,7 @@
 #include "synkpar/mlp.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <random>
 
 #include "internal.hpp"
@@ -71,12 +72,44 @@ DevBuffer as_dtype(const std::shared_ptr<detail::RankDevice>& rd, const DevBuffe
     return out;
 }
 
+// The rank's bf16 weight shadow of `pvar` for these dims (synk_cuda.h):
+// (re)allocated when missing or of another shape; *valid = it still equals
+// bf16(params) (made at the variable's current epoch from this storage).
+void* weight_shadow(const ReplicatedVariable& pvar, const std::shared_ptr<detail::RankDevice>& rd,
+                    const DevBuffer& params, const std::vector<std::uint64_t>& dims, int* valid) {
+    detail::VarRecord& rec = detail::record_of(pvar);
+    const std::size_t r = rd->rank;
+    *valid = 0;
+    if (const char* e = std::getenv("SYNK_MLP_SHADOW"); e && e[0] == '0') return nullptr;  // A/B and tests
+    if (r >= rec.shadows.size() || r >= rec.replicas.size() || rec.replicas[r].data() != params.data()) return nullptr;
+    detail::VarRecord::Bf16Shadow& sh = rec.shadows[r];
+    if (sh.dims != dims || !sh.buf.has_storage() || sh.buf.owner().get() != rd.get()) {
+        synk_bf16_shadow layout{};
+        if (synk_mlp_bf16_shadow(dims.data(), static_cast<std::uint32_t>(dims.size() - 1), &layout) != SYNK_OK)
+            return nullptr;  // more layers than the shadow supports: the casts go to the workspace
+        sh.buf = DevBuffer::alloc(rd, {(layout.bytes + 7) / 8}, DType::Float64);  // bytes; dtype is bookkeeping
+        sh.layout = layout;
+        sh.dims = dims;
+        sh.epoch = ~std::uint64_t(0);
+    }
+    *valid = sh.epoch == rec.epoch.load() && sh.params == params.data();
+    return sh.buf.data();
+}
+
+void mark_shadow_current(const ReplicatedVariable& pvar, std::size_t rank, const DevBuffer& params) {
+    detail::VarRecord& rec = detail::record_of(pvar);
+    detail::VarRecord::Bf16Shadow& sh = rec.shadows[rank];
+    sh.epoch = rec.epoch.load();
+    sh.params = params.data();
+}
+
 // Enqueue loss + gradient on rd's stream. Returns (loss f64 scalar, grad).
 std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::RankDevice>& rd, const Checked& c,
                                                  const DevBuffer& params, const DevBuffer& x, const DevBuffer& y,
                                                  MlpCompute compute = MlpCompute::Native,
                                                  const KernelContext* ctx = nullptr,
-                                                 const std::uint64_t* rows = nullptr) {
+                                                 const KernelContext::IndexedInput* rows = nullptr,
+                                                 const ReplicatedVariable* pvar = nullptr) {
     const DType dt = params.dtype();
     if (compute == MlpCompute::Bf16TensorCore && dt != DType::Float32)
         throw DTypeError("mlp_grad_kernel: bf16 tensor-core compute needs float32 parameters");
@@ -89,12 +122,23 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     void* ws = detail::rank_scratch(rd, ws_bytes);
     DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
     DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
-    const int base = ctx && ctx->grad_segments ? ctx->grad_signal_base : -1;
+    synk_mlp_opts opts{};
+    opts.signal_base = ctx && ctx->grad_segments ? ctx->grad_signal_base : -1;
+    const int base = opts.signal_base;
+    if (rows) {
+        opts.rows = rows->rows;
+        opts.rows_host = rows->host_rows;
+        opts.rows_ready_on = rows->ready_on;
+        opts.rows_ready_slot = rows->ready_slot;
+    }
+    const bool shadowed = pvar && compute == MlpCompute::Bf16TensorCore;
+    if (shadowed) opts.shadow = weight_shadow(*pvar, rd, params, c.dims, &opts.shadow_valid);
     int signalled = 0;
-    detail::check(synk_mlp_loss_grad_seg(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(), xd.data(),
-                                         yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws, ws_bytes,
-                                         base, &signalled, rows),
+    detail::check(synk_mlp_loss_grad_opts(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(),
+                                          xd.data(), yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws,
+                                          ws_bytes, &opts, &signalled),
                   "mlp_loss_grad");
+    if (opts.shadow) mark_shadow_current(*pvar, rd->rank, params);
     if (signalled > 0) {
         // Layer l's segment [W_l, b_l] was signalled on slot base + l, in
         // backward order (l = L-1 ... 0); W_l and b_l are adjacent in the layout.
@@ -204,7 +248,8 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
         r.updates.push_back(UpdateDelta{grads_id, detail::dev_to_host(grad), UpdateCombine::WeightedMeanByRows});
         return r;
     };
-    k.device_fn = [segs, grads_id, compute](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
+    const ReplicatedVariable pvar = block.params;
+    k.device_fn = [segs, grads_id, compute, pvar](const std::vector<DevBuffer>& in, const KernelContext& ctx) {
         const DevBuffer& params = ctx.device_replica(0);
         const KernelContext::IndexedInput* ix = ctx.indexed ? &(*ctx.indexed)[0] : nullptr;
         const KernelContext::IndexedInput* iy = ctx.indexed ? &(*ctx.indexed)[1] : nullptr;
@@ -216,7 +261,7 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
                                 (compute == MlpCompute::Native || params.dtype() == DType::Float32);
             if (direct) {
                 c.n = ix->count;
-                auto [loss, grad] = device_loss_grad(rd, c, params, in[0], in[1], compute, &ctx, ix->rows);
+                auto [loss, grad] = device_loss_grad(rd, c, params, in[0], in[1], compute, &ctx, ix, &pvar);
                 DeviceKernelResult r;
                 r.outputs.push_back(loss);
                 r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
@@ -225,6 +270,8 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
             // Gather the selected rows here, then the regular path.
             auto gathered = [&](const DevBuffer& src, const KernelContext::IndexedInput& sel) {
                 if (!sel.rows) return src;
+                if (sel.ready_on)
+                    detail::check(synk_wait_peer_slot(rd->h, sel.ready_on, sel.ready_slot), "mlp: index stage wait");
                 std::vector<std::size_t> shape = src.shape();
                 shape[0] = sel.count;
                 DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
@@ -235,14 +282,14 @@ Kernel mlp_grad_kernel(const FlatParamBlock& block, std::string name, MlpCompute
             };
             const DevBuffer xg = gathered(in[0], *ix), yg = gathered(in[1], *iy);
             Checked cg = check_operands(params, segs, xg, yg);
-            auto [loss, grad] = device_loss_grad(rd, cg, params, xg, yg, compute, &ctx);
+            auto [loss, grad] = device_loss_grad(rd, cg, params, xg, yg, compute, &ctx, nullptr, &pvar);
             DeviceKernelResult r;
             r.outputs.push_back(loss);
             r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});
             return r;
         }
         Checked c = check_operands(params, segs, in[0], in[1]);
-        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute, &ctx);
+        auto [loss, grad] = device_loss_grad(ctx.rank_device, c, params, in[0], in[1], compute, &ctx, nullptr, &pvar);
         DeviceKernelResult r;
         r.outputs.push_back(loss);
         r.updates.push_back({grads_id, grad, UpdateCombine::WeightedMeanByRows});

@@ -111,6 +111,7 @@ ReplicatedVariable replicate(WorkerPool& pool, const NdBuffer& init) {
     rec->id = g_next_var.fetch_add(1);
     rec->pool = st;
     rec->replicas.resize(st->world);
+    rec->shadows.resize(st->world);
     detail::run_pool_phase(*st, PhaseKind::Distribute, [&](std::size_t r) {
         rec->replicas[r] = detail::dev_from_host(st->ranks[r], init);
         detail::dev_sync(st->ranks[r]);
@@ -124,6 +125,7 @@ DType ReplicatedVariable::dtype() const { return live(rec_, "dtype").replicas.at
 
 void ReplicatedVariable::broadcast(std::size_t src) {
     detail::VarRecord& rec = live(rec_, "broadcast");
+    rec.mutated();
     check_rank(rec, src, "broadcast");
     detail::PoolState& st = *rec.pool;
     detail::require_idle(st, "broadcast");
@@ -167,6 +169,7 @@ void ReplicatedVariable::broadcast(std::size_t src) {
 
 void ReplicatedVariable::all_reduce(ReduceOp op) {
     detail::VarRecord& rec = live(rec_, "all_reduce");
+    rec.mutated();
     not_gather(op, "all_reduce");
     check_same_shapes(rec, "all_reduce");
     detail::PoolState& st = *rec.pool;
@@ -205,6 +208,7 @@ void ReplicatedVariable::all_reduce(ReduceOp op) {
 
 void ReplicatedVariable::reduce(ReduceOp op, std::size_t dst) {
     detail::VarRecord& rec = live(rec_, "reduce");
+    rec.mutated();
     not_gather(op, "reduce");
     check_rank(rec, dst, "reduce");
     check_same_shapes(rec, "reduce");
@@ -283,6 +287,7 @@ NdBuffer ReplicatedVariable::get_value(std::size_t rank) const {
 
 void ReplicatedVariable::set_value(std::size_t rank, const NdBuffer& value) {
     detail::VarRecord& rec = live(rec_, "set_value");
+    rec.mutated();
     check_rank(rec, rank, "set_value");
     no_phase(rec, "set_value");
     const auto& rd = rec.pool->ranks[rank];
@@ -293,6 +298,7 @@ void ReplicatedVariable::set_value(std::size_t rank, const NdBuffer& value) {
 
 void ReplicatedVariable::scatter_value(const NdBuffer& data, const std::optional<IndexSelection>& indexes) {
     detail::VarRecord& rec = live(rec_, "scatter_value");
+    rec.mutated();
     const std::size_t n = data.rows();
     std::size_t eff = n;
     if (indexes) {
@@ -315,6 +321,7 @@ void ReplicatedVariable::scatter_value(const SharedInputArray& data, const std::
 
 void ReplicatedVariable::scatter_uniform(const std::vector<std::size_t>& shape, DType dtype, std::uint64_t seed) {
     detail::VarRecord& rec = live(rec_, "scatter_uniform");
+    rec.mutated();
     if (shape.empty()) throw ShapeError("scatter_uniform: a rank-0 shape has no rows to scatter");
     const std::size_t row = element_count(shape) / std::max<std::size_t>(shape[0], 1);
     std::vector<RowRange> parts = partition_rows(shape[0], rec.replicas.size());
@@ -348,6 +355,7 @@ bool ReplicatedVariable::replicas_coherent() const {
 
 DevBuffer ReplicatedVariable::device_value(std::size_t rank) const {
     detail::VarRecord& rec = live(rec_, "device_value");
+    rec.mutated();
     check_rank(rec, rank, "device_value");
     return rec.replicas[rank];
 }

@@ -267,6 +267,7 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     constexpr int kSegBase = 1, kAuxDone = 63;
     std::vector<std::size_t> seg_counts(W, 0);
     std::vector<char> seg_cover(W, 0);
+    std::vector<char> shadow_written(W, 0);
     const std::size_t n_total = grads[0].size();
 
     auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows, const std::vector<GradSegment>& segs) {
@@ -317,6 +318,24 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
         }
         bool overlap = !unequal;
         for (std::size_t p = 0; p < W; ++p) overlap = overlap && seg_cover[p] && seg_counts[p] == segs.size();
+        // bf16 weight shadows (the bf16 MLP's operand copies, one per rank):
+        // when every rank holds a current one, the update writes them along
+        // with the new params and the next step skips its weight casts. Read
+        // after the rendezvous, when every rank has made its own.
+        const synk_bf16_shadow* shl = nullptr;
+        std::vector<void*> shb(W, nullptr);
+        {
+            detail::VarRecord& prec = detail::record_of(block_.params);
+            bool ok = W <= SYNK_SHADOW_MAX_WORLD && prec.shadows.size() == W && dt == SYNK_F32;
+            for (std::size_t p = 0; p < W && ok; ++p) {
+                const detail::VarRecord::Bf16Shadow& sh = prec.shadows[p];
+                ok = sh.buf.has_storage() && sh.params == pp[p] && sh.epoch == prec.epoch.load() &&
+                     sh.dims == prec.shadows[0].dims;
+                shb[p] = ok ? sh.buf.data() : nullptr;
+            }
+            if (ok) shl = &prec.shadows[0].layout;
+            shadow_written[r] = ok;
+        }
         // The gradient update may have swapped each rank's grads replica for a
         // fresh buffer (WeightedMeanByRows adopts its accumulator): read the
         // pointers only now, after every rank applied its update.
@@ -329,10 +348,10 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             // W = 1: the update directly follows the compute end (event 3) on this stream
             if (r == 0 && t0_timer && W > 1) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
             if (r == 0) update_from_compute_end_ = W == 1;
-            detail::check(synk_all_reduce_step(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
-                                               hyper.data(), lr_, t_next, pp.data(), gp.data(),
-                                               a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
-                                               grads[r].size(), coherent ? 1 : 0),
+            detail::check(synk_all_reduce_step_ex(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
+                                                  hyper.data(), lr_, t_next, pp.data(), gp.data(),
+                                                  a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
+                                                  grads[r].size(), coherent ? 1 : 0, 0, shl, shb.data()),
                           "fused all-reduce + update");
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
             if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 5), "timer");
@@ -357,10 +376,10 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             if (r == 0 && t0_timer && k == 0) detail::check(synk_timer_record(aux, t0_timer, 4), "timer");
             if (r == 0 && k == 0) update_from_compute_end_ = false;
             std::vector<void*> ps = at(pp, g.first), gs = at(gp, g.first), x0 = at(a0, g.first), x1 = at(a1, g.first);
-            detail::check(synk_all_reduce_step(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
-                                               hyper.data(), lr_, t_next, ps.data(), gs.data(),
-                                               a0.empty() ? nullptr : x0.data(), a1.empty() ? nullptr : x1.data(),
-                                               g.count, coherent ? 1 : 0),
+            detail::check(synk_all_reduce_step_ex(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
+                                                  hyper.data(), lr_, t_next, ps.data(), gs.data(),
+                                                  a0.empty() ? nullptr : x0.data(), a1.empty() ? nullptr : x1.data(),
+                                                  g.count, coherent ? 1 : 0, g.first, shl, shb.data()),
                           "segment all-reduce + update");
         }
         if (r == 0 && timing) detail::check(synk_mark(aux, &mb), "mark");
@@ -385,8 +404,18 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     }
     rep.step_call.rank_rows.assign(W, 1);
     detail::record_of(block_.grads).coherent = true;
-    detail::record_of(block_.params).coherent = true;
-    for (const ReplicatedVariable& a : aux_) detail::record_of(a).coherent = true;
+    detail::record_of(block_.grads).mutated();
+    detail::VarRecord& prec = detail::record_of(block_.params);
+    prec.coherent = true;
+    prec.mutated();
+    bool all_shadows = true;
+    for (std::size_t r = 0; r < W; ++r) all_shadows = all_shadows && shadow_written[r];
+    if (all_shadows)  // the update wrote every rank's shadow with the new params
+        for (auto& sh : prec.shadows) sh.epoch = prec.epoch.load();
+    for (const ReplicatedVariable& a : aux_) {
+        detail::record_of(a).coherent = true;
+        detail::record_of(a).mutated();
+    }
     t_ += 1;
     if (opts_.verify_coherence && !block_.params.replicas_coherent())
         throw CoherenceError("train_step(): parameter replicas diverged after step " + std::to_string(t_));
@@ -487,6 +516,8 @@ double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<Fun
                           "fused all-reduce + update");
             detail::dev_sync(rd);
         });
+        detail::record_of(block_.params).mutated();
+        for (const ReplicatedVariable& a : aux_) detail::record_of(a).mutated();
         rep.allreduce_s = since(ta);
         rep.step_call.rank_compute_s = ph2.rank_seconds;
         rep.step_call.rank_rows.assign(W, 1);

@@ -92,3 +92,46 @@ def test_pageable_source_index_list(sk, oracle, world):
             f.call([src], indexes=bad)
         (again,) = f.call([src], indexes=idx[::-1].copy())
         assert again.tobytes() == oracle.gather_rows(src, idx[::-1].astype(np.uint64)).tobytes()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_bf16_weight_shadow_bitwise_and_invalidation(sk, world):
+    """The bf16 MLP's weight shadow (bf16 operand copies written by the fused
+    update, so the next step skips the weight casts) changes no bit: the
+    trajectory equals the one with the casts every step (SYNK_MLP_SHADOW=0),
+    also across parameter writes that must invalidate it (set_value,
+    broadcast) and an unequal-shard step (pre-scale path)."""
+    import os
+
+    cfg = sk.MlpConfig(in_dim=192, width=320, out_dim=100, layers=3, seed=11)
+    x, y = sk.mlp_make_dataset(1024, cfg, seed=12, dtype="f32")
+    runs = {}
+    for shadow in ("1", "0"):
+        os.environ["SYNK_MLP_SHADOW"] = shadow
+        try:
+            with sk.Pool(workers=world) as pool:
+                sx, sy = sk.SharedInput.from_array(x), sk.SharedInput.from_array(y)
+                sx.mirror(pool)
+                sy.mirror(pool)
+                block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+                f = sk.mlp_grad_function(pool, block, compute="bf16")
+                sk.distribute(pool)
+                tr = sk.Trainer(pool, block, sk.MomentumRule(), lr=1e-2, verify_coherence=True)
+                rng = np.random.default_rng(3)
+                losses = []
+                for step in range(7):
+                    if step == 3:  # an outside write: every shadow must be rebuilt
+                        p = block.params.get(0)
+                        p[:50] += np.float32(0.25)
+                        for r in range(world):
+                            block.params.set(r, p)
+                    if step == 5 and world > 1:
+                        block.params.broadcast(world - 1)
+                    n = 256 * world + (3 if step == 4 else 0)  # step 4: unequal shards
+                    losses.append(tr.train_step(f, [sx, sy], indexes=rng.integers(0, 1024, n)))
+                runs[shadow] = (losses, block.params.get(world - 1).tobytes(), block.grads.get(0).tobytes())
+        finally:
+            os.environ.pop("SYNK_MLP_SHADOW", None)
+    assert runs["1"][0] == runs["0"][0]
+    assert runs["1"][1] == runs["0"][1]
+    assert runs["1"][2] == runs["0"][2]

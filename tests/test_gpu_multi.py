@@ -67,10 +67,11 @@ def test_p2p_collectives_bitwise_across_gpus(sk, ngpu):
                 for r in range(world):
                     v.set(r, vals[r])
                 v.reduce("sum", world - 1)
-                assert v.get(world - 1).tobytes() == g["reduce_sum_%s_w%d" % (tag, world)].tobytes()
-                v.broadcast(world - 1)
+                folded = g["reduce_sum_%s_w%d" % (tag, world)].tobytes()
+                assert v.get(world - 1).tobytes() == folded
+                v.broadcast(world - 1)  # the reduced replica goes to every GPU
                 for r in range(world):
-                    assert v.get(r).tobytes() == vals[world - 1].tobytes()
+                    assert v.get(r).tobytes() == folded
 
 
 @pytest.mark.parametrize("n", [1000, (1 << 22) + 5])
