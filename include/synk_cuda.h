@@ -239,14 +239,21 @@ int synk_optimizer_step(synk_dev* dev, int dtype, int rule, const double* hyper,
  * writes the reduced chunk back to every gradient replica, applies the rule
  * to chunk r of its own params/aux and stores the new chunk into every
  * params/aux replica. aux0/aux1 may be NULL for rules without state.
- * replicas_coherent = 1 promises that params/aux replicas are bitwise equal
- * (the executor tracks this), so chunk r is computed once from rank r's
- * replica; with 0 every replica's chunk is updated from its own values,
- * exactly as per-rank steps would (sgd.cpp:226-248). */
+ * flags: SYNK_STEP_COHERENT promises that params/aux replicas are bitwise
+ * equal (the executor tracks this), so chunk r is computed once from rank r's
+ * replica; without it every replica's chunk is updated from its own values,
+ * exactly as per-rank steps would (sgd.cpp:226-248). SYNK_STEP_GRADS_LOCAL
+ * (world > 1) writes the reduced gradient chunk r into rank r's gradient
+ * replica only -- a deferred all-gather: replica q then holds the reduced
+ * values in chunk q alone (synk_chunk_range), and the caller pulls the other
+ * chunks before anything reads the gradients (NVLink bytes per rank per step
+ * 2(W-1)/W * S instead of 3(W-1)/W * S). */
+#define SYNK_STEP_COHERENT 1
+#define SYNK_STEP_GRADS_LOCAL 2
 int synk_all_reduce_step(synk_dev* dev, int world, int dtype, int grad_op, int rule,
                          const double* hyper, double lr, uint64_t t, void* const* params,
                          void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
-                         int replicas_coherent);
+                         int flags);
 
 /* ---- tensor-core GEMM (the MLP's dense products, mlp.cpp:31-73) -------------------- */
 #define SYNK_BF16 3     /* storage code for bf16 operands/outputs (new; DType has f32/f64) */
@@ -318,7 +325,7 @@ int synk_mlp_bf16_shadow(const uint64_t* dims, uint32_t layers, synk_bf16_shadow
 int synk_all_reduce_step_ex(synk_dev* dev, int world, int dtype, int grad_op, int rule,
                             const double* hyper, double lr, uint64_t t, void* const* params,
                             void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
-                            int replicas_coherent, uint64_t elem_base, const synk_bf16_shadow* shadow,
+                            int flags, uint64_t elem_base, const synk_bf16_shadow* shadow,
                             void* const* shadow_bases);
 
 #define SYNK_GEMM_A_MN 1
@@ -354,15 +361,20 @@ int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t
  *   signal_base      as synk_mlp_loss_grad_seg (-1: no segment signals)
  *   rows             index-fused batch rows in HBM (as synk_mlp_loss_grad_seg)
  *   rows_host        the same list as a device-readable alias of page-locked
- *                    host memory, or NULL: the bf16 x staging may read it in
- *                    place instead of waiting for `rows` to be filled
+ *                    host memory, or NULL (informational: the x staging
+ *                    reads `rows`, PCIe latency per tile made it slower)
  *   rows_ready_on / rows_ready_slot: `rows` is filled once the slot event of
  *                    that handle fires (synk_signal_slot); the stream waits on
  *                    it before the first read of `rows`. NULL: ready now.
  *   shadow           bf16 weight shadow (synk_mlp_bf16_shadow layout) of this
  *                    rank, bf16 path only; NULL: casts into the workspace
  *   shadow_valid     1: the shadow equals bf16(params): the casts are skipped;
- *                    0: the casts write the shadow (valid afterwards). */
+ *                    0: the casts write the shadow (valid afterwards).
+ *   shadow_spare     1: the update that follows writes the NEXT shadow into
+ *                    another buffer (double-buffered shadows), so segment l is
+ *                    signalled right after its weight gradient; 0: the update
+ *                    rewrites this shadow, so segment l (l > 0) is signalled
+ *                    only after dX_l has read W_l. */
 typedef struct synk_mlp_opts {
     int signal_base;
     const uint64_t* rows;
@@ -371,6 +383,7 @@ typedef struct synk_mlp_opts {
     int rows_ready_slot;
     void* shadow;
     int shadow_valid;
+    int shadow_spare;
 } synk_mlp_opts;
 int synk_mlp_loss_grad_opts(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                             const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,

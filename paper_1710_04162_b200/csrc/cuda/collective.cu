@@ -258,7 +258,7 @@ __device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t g
 template <class T, int W, int BYTES, bool SH>
 __device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
                                             int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
-                                            int naux, uint64_t v, const Shadow& sh) {
+                                            int naux, uint64_t v, const Shadow& sh, bool grads_local) {
     using V = VecT<T, BYTES>;
     constexpr int N = V::N;
     V gx[W];
@@ -273,8 +273,12 @@ __device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grad
         g.e[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
     }
     if constexpr (W > 1) {
+        if (grads_local) {  // deferred all-gather: the chunk stays with its owner
+            vstore<T, BYTES>(grads.p[rank], v, g);
+        } else {
 #pragma unroll
-        for (int q = 0; q < W; ++q) vstore<T, BYTES>(grads.p[q], v, g);
+            for (int q = 0; q < W; ++q) vstore<T, BYTES>(grads.p[q], v, g);
+        }
     }
     V p = vload<T, BYTES>(params.p[rank], v);
     V a0 = naux > 0 ? vload<T, BYTES>(aux0.p[rank], v) : p;
@@ -301,7 +305,8 @@ __device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grad
 template <class T, int W, bool SH>
 __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
-    double inv_w, synk::RuleParams rp, int naux, bool coherent, uint64_t lo, uint64_t hi, int vec_bytes, Shadow sh) {
+    double inv_w, synk::RuleParams rp, int naux, bool coherent, bool grads_local, uint64_t lo, uint64_t hi,
+    int vec_bytes, Shadow sh) {
     const int fop = grad_op == SYNK_OP_MEAN ? SYNK_OP_SUM : grad_op;
     uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     uint64_t stride = (uint64_t)gridDim.x * kBlock;
@@ -312,13 +317,15 @@ __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
                 constexpr int N = VecT<T, 32>::N;
                 const uint64_t v0 = lo / N, v1 = hi / N;
                 for (uint64_t v = v0 + tid; v < v1; v += stride)
-                    step_vector<T, W, 32, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh);
+                    step_vector<T, W, 32, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh,
+                                              grads_local);
                 lo = v1 * N;  // scalar tail below
             } else {
                 constexpr int N = VecT<T, 16>::N;
                 const uint64_t v0 = lo / N, v1 = hi / N;
                 for (uint64_t v = v0 + tid; v < v1; v += stride)
-                    step_vector<T, W, 16, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh);
+                    step_vector<T, W, 16, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh,
+                                              grads_local);
                 lo = v1 * N;
             }
         }
@@ -330,12 +337,18 @@ __global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
 #pragma unroll
             for (int q = 0; q < W; ++q) e[q] = static_cast<const T*>(grads.p[q])[i];
             g = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
+            if (grads_local) {
+                static_cast<T*>(grads.p[rank])[i] = g;
+            } else {
 #pragma unroll
-            for (int q = 0; q < W; ++q) static_cast<T*>(grads.p[q])[i] = g;
+                for (int q = 0; q < W; ++q) static_cast<T*>(grads.p[q])[i] = g;
+            }
         } else {
             for (int q = 0; q < world; ++q) e[q] = static_cast<const T*>(grads.p[q])[i];
             g = finish_mean(grad_op, tree_fold_dyn(fop, e, world), inv_w);
-            for (int q = 0; q < world; ++q) static_cast<T*>(grads.p[q])[i] = g;
+            if (grads_local) static_cast<T*>(grads.p[rank])[i] = g;
+            else
+                for (int q = 0; q < world; ++q) static_cast<T*>(grads.p[q])[i] = g;
         }
         const double gd = (double)g;
         if (coherent) {
@@ -446,7 +459,9 @@ bool ptrs_aligned(void* const* bufs, int w, uintptr_t align) {
 template <class T>
 int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp, void* const* params,
                      void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,
-                     bool coherent, const Shadow* sh) {
+                     int flags, const Shadow* sh) {
+    const bool coherent = flags & SYNK_STEP_COHERENT;
+    const bool grads_local = (flags & SYNK_STEP_GRADS_LOCAL) && w > 1;
     Ptrs P{}, G{}, A0{}, A1{};
     int naux = synk::rule_aux_count(rp.rule);
     if (int rc = fill_ptrs(&P, params, w); rc != SYNK_OK) return rc;
@@ -484,10 +499,10 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     case WW:                                                                                                     \
         if (with)                                                                                                \
             allreduce_step_kernel<T, WW, true><<<grid, kBlock, 0, d->stream>>>(                                  \
-                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec_bytes, S);             \
+                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
         else                                                                                                     \
             allreduce_step_kernel<T, WW, false><<<grid, kBlock, 0, d->stream>>>(                                 \
-                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, lo, hi, vec_bytes, S);             \
+                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
         break;
         SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(3) SYNK_ARS_CASE(4)
         SYNK_ARS_CASE(5) SYNK_ARS_CASE(6) SYNK_ARS_CASE(7) SYNK_ARS_CASE(8)
@@ -495,7 +510,8 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     default:
         SYNK_REQUIRE(!with, SYNK_EARG, "all_reduce_step: bf16 shadows need world <= 8");
         allreduce_step_kernel<T, 0, false><<<grid, kBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
-                                                                           inv_w, rp, naux, coherent, lo, hi, 0, S);
+                                                                           inv_w, rp, naux, coherent, grads_local, lo, hi, 0,
+                                                                           S);
     }
     SYNK_LAUNCHED("allreduce_step_kernel");
     return SYNK_OK;
@@ -620,7 +636,7 @@ int synk_optimizer_step(synk_dev* d, int dtype, int rule, const double* hyper, d
 
 int synk_all_reduce_step(synk_dev* d, int world, int dtype, int grad_op, int rule, const double* hyper,
                          double lr, uint64_t t, void* const* params, void* const* grads,
-                         void* const* aux0, void* const* aux1, uint64_t n, int coherent) {
+                         void* const* aux0, void* const* aux1, uint64_t n, int flags) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "synk_all_reduce_step: bad dtype");
     SYNK_REQUIRE(grad_op >= SYNK_OP_SUM && grad_op <= SYNK_OP_PROD, SYNK_EARG,
                  "all_reduce: Gather is not a reduction (use gather())");
@@ -629,17 +645,17 @@ int synk_all_reduce_step(synk_dev* d, int world, int dtype, int grad_op, int rul
     if (n == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     return dtype == SYNK_F32
-               ? allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, nullptr)
-               : allreduce_step_t<double>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, nullptr);
+               ? allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, flags, nullptr)
+               : allreduce_step_t<double>(d, world, grad_op, rp, params, grads, aux0, aux1, n, flags, nullptr);
 }
 
 int synk_all_reduce_step_ex(synk_dev* d, int world, int dtype, int grad_op, int rule, const double* hyper,
                             double lr, uint64_t t, void* const* params, void* const* grads,
-                            void* const* aux0, void* const* aux1, uint64_t n, int coherent, uint64_t elem_base,
+                            void* const* aux0, void* const* aux1, uint64_t n, int flags, uint64_t elem_base,
                             const synk_bf16_shadow* shadow, void* const* shadow_bases) {
     if (!shadow)
         return synk_all_reduce_step(d, world, dtype, grad_op, rule, hyper, lr, t, params, grads, aux0, aux1, n,
-                                    coherent);
+                                    flags);
     SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EDTYPE, "all_reduce_step: bf16 shadows need f32 params");
     SYNK_REQUIRE(world >= 1 && world <= SYNK_SHADOW_MAX_WORLD, SYNK_EARG, "all_reduce_step: shadows need world <= 8");
     SYNK_REQUIRE(shadow->count <= SYNK_SHADOW_MAX_SEGS && shadow_bases, SYNK_EARG, "all_reduce_step: bad shadow");
@@ -657,7 +673,7 @@ int synk_all_reduce_step_ex(synk_dev* d, int world, int dtype, int grad_op, int 
     S.elem_base = elem_base;
     for (uint32_t k = 0; k < shadow->count; ++k) S.seg[k] = shadow->seg[k];
     synk::DeviceGuard g(d->device);
-    return allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, coherent, &S);
+    return allreduce_step_t<float>(d, world, grad_op, rp, params, grads, aux0, aux1, n, flags, &S);
 }
 
 }  // extern "C"

@@ -11,6 +11,7 @@
 // This file holds the SIMT path (FFMA for f32, DFMA for f64 — the f64 path
 // is what the reference's f64 trajectories are checked against at 1e-10).
 
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -489,12 +490,13 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         rows_waited = true;
         return synk_wait_peer_slot(d, opts->rows_ready_on, opts->rows_ready_slot);
     };
+    // The x staging reads the HBM copy of the list: read in place over PCIe
+    // (rows_host) every 64x64 tile re-fetched its 64 indices at PCIe latency,
+    // 121 us instead of 27 us for the C5 batch (profiles/r02_c5_trace.txt),
+    // far more than the 7.5 us stage copy it would hide.
     const uint64_t* xrows = rows;
-    if (rows && opts && opts->rows_host) {
-        xrows = opts->rows_host;  // the x staging reads the list over PCIe, no wait for the stage copy
-    } else if (rows) {
+    if (rows)
         if (int rc = wait_rows(); rc) return rc;
-    }
     // input batch: x and x^T in bf16 (rows != null: gathered from the whole source in the same pass)
     if (int rc = synk_gemm_prep2_bf16_rows(d, x, xrows, n, dims[0], dims[0], bf(B.off_act[0]), pad8(dims[0]),
                                            bf(B.off_actT[0]), pad8(n));
@@ -553,9 +555,10 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         // Segment [W_l, b_l] of the gradient is final, and the f32 W_l/b_l are
         // not read again in this pass (the GEMMs read the bf16 copies made at
         // the start): the trainer may all-reduce + update it from here on --
-        // unless the bf16 copy is the rank's shadow, which that update
-        // rewrites: then only after dX_l below has read W_l.
-        if (signal_base >= 0 && (!shb || l == 0))
+        // unless the bf16 copy is the rank's shadow and that update rewrites
+        // it in place (no spare): then only after dX_l below has read W_l.
+        const bool late = shb && !opts->shadow_spare;
+        if (signal_base >= 0 && (!late || l == 0))
             if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
         if (l > 0) {
             // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
@@ -568,7 +571,7 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
                 rc)
                 return rc;
             cur = nxt;
-            if (signal_base >= 0 && shb)
+            if (signal_base >= 0 && late)
                 if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
         }
     }
@@ -635,6 +638,14 @@ int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
         gc.disabled = true;
         return launch_all();
     }
+    static const bool debug = [] {
+        const char* e = getenv("SYNK_DEBUG_GRAPHS");  // diagnostics: report every capture
+        return e && e[0] == '1';
+    }();
+    if (debug)
+        fprintf(stderr, "[synk] mlp graph capture rank %d (%zu cached, miss %d): p=%p x=%p y=%p loss=%p g=%p ws=%p rows=%p\n",
+                d->rank, gc.entries.size(), gc.misses_in_a_row, key.ptrs[0], key.ptrs[1], key.ptrs[2], key.ptrs[3],
+                key.ptrs[4], key.ptrs[5], key.ptrs[6]);
     cudaGraph_t graph = nullptr;
     SYNK_CU(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
     const int rc = launch_all();

@@ -31,7 +31,37 @@ synk_dev* RankDevice::aux_handle() {
     return aux;
 }
 
+void* RankDevice::take_block(std::size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lock(cache_mu);
+        auto it = cache.find(bytes);
+        if (it != cache.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            cache_bytes -= bytes;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    check(synk_alloc(h, bytes, &p), "HBM allocation");
+    return p;
+}
+
+void RankDevice::release_block(void* ptr, std::size_t bytes) {
+    if (bytes <= kCacheMaxBlock) {
+        std::lock_guard<std::mutex> lock(cache_mu);
+        if (cache_bytes + bytes <= kCacheMaxBytes) {
+            cache[bytes].push_back(ptr);
+            cache_bytes += bytes;
+            return;
+        }
+    }
+    synk_free(h, ptr);  // stream-ordered; errors at teardown are moot
+}
+
 RankDevice::~RankDevice() {
+    for (auto& [bytes, list] : cache)
+        for (void* p : list) synk_free(h, p);
     if (aux) synk_close(aux);
     if (h && index_stage) synk_free(h, index_stage);
     if (staging) synk_host_free(staging);
@@ -51,7 +81,7 @@ void* rank_scratch(const std::shared_ptr<RankDevice>& rd, std::size_t bytes) {
 }
 
 DevStorage::~DevStorage() {
-    if (ptr && owner) synk_free(owner->h, ptr);  // stream-ordered; errors at teardown are moot
+    if (ptr && owner) owner->release_block(ptr, bytes);
 }
 
 int synk_dtype(DType dt) { return dt == DType::Float32 ? SYNK_F32 : SYNK_F64; }
@@ -123,7 +153,7 @@ DevBuffer DevBuffer::alloc(const std::shared_ptr<detail::RankDevice>& owner, std
     auto st = std::make_shared<detail::DevStorage>();
     st->owner = owner;
     st->bytes = b.byte_size();
-    if (st->bytes) detail::check(synk_alloc(owner->h, st->bytes, &st->ptr), "HBM allocation");
+    if (st->bytes) st->ptr = owner->take_block(st->bytes);
     b.store_ = std::move(st);
     return b;
 }

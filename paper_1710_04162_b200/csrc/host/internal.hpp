@@ -7,8 +7,10 @@
 #include <istream>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "synk_cuda.h"
@@ -52,6 +54,18 @@ struct RankDevice {
     // DevBuffer here would keep its own RankDevice alive.
     void* index_stage = nullptr;
     std::size_t index_stage_bytes = 0;
+    // Freed HBM blocks of this rank by exact size, reused last-in first-out:
+    // a rank gets back the block it released last whatever other ranks on the
+    // same GPU allocate meanwhile, so per-step buffers (a kernel's gradient
+    // and loss) cycle through the same few addresses and the CUDA graphs
+    // keyed on them keep hitting. Bounded; larger blocks go back to the pool.
+    static constexpr std::size_t kCacheMaxBlock = std::size_t(64) << 20;
+    static constexpr std::size_t kCacheMaxBytes = std::size_t(512) << 20;
+    std::mutex cache_mu;
+    std::unordered_map<std::size_t, std::vector<void*>> cache;
+    std::size_t cache_bytes = 0;
+    void* take_block(std::size_t bytes);             // cached block or a fresh allocation
+    void release_block(void* ptr, std::size_t bytes);
     ~RankDevice();
 };
 
@@ -100,18 +114,42 @@ struct VarRecord {
     std::atomic<std::uint64_t> epoch{0};
     // Per rank: bf16 copy of an MLP's weights in the tensor-core operand
     // layout (synk_mlp_bf16_shadow), made by the bf16 MLP kernel and kept
-    // current by the trainer's fused update. Slot r is touched only by rank
-    // r's thread (or the master between phases).
+    // current by the trainer's fused update. Double-buffered: the kernel
+    // reads buf[cur] while the update writes the next step's copy into
+    // buf[cur ^ 1] (so a layer's update may start as soon as its weight
+    // gradient is final), then the trainer flips cur. Slot r is touched only
+    // by rank r's thread (or the master between phases).
     struct Bf16Shadow {
-        DevBuffer buf;
-        std::uint64_t epoch = ~std::uint64_t(0);  // VarRecord::epoch it matches
+        DevBuffer buf[2];
+        int cur = 0;
+        std::uint64_t epoch = ~std::uint64_t(0);  // VarRecord::epoch buf[cur] matches
         const void* params = nullptr;             // the replica storage it mirrors
         std::vector<std::uint64_t> dims;
         synk_bf16_shadow layout{};
     };
     std::vector<Bf16Shadow> shadows;
+    // Deferred all-gather of a reduced gradient (the trainer's fused step with
+    // SYNK_STEP_GRADS_LOCAL): for every segment (first, count), replica q
+    // holds the reduced values only in its own chunk (synk_chunk_range of
+    // count). `src` keeps the buffers those chunks live in alive and
+    // unwritten; a replica swapped for fresh storage since (an Overwrite /
+    // WeightedMeanByRows update, set_value) is complete and needs nothing.
+    // Readers complete the rest first: materialize() on the master between
+    // phases, pull_shard() by a rank inside a phase.
+    struct Shard {
+        std::vector<DevBuffer> src;
+        std::vector<std::pair<std::uint64_t, std::uint64_t>> segs;
+    };
+    std::optional<Shard> shard;
     void mutated() { epoch.fetch_add(1); }
 };
+
+// Complete every replica of a sharded variable (master thread, no phase in
+// flight); a no-op otherwise.
+void materialize(VarRecord& rec);
+// Rank r's part of it, enqueued on r's stream (inside a phase: reads only the
+// retained chunk owners, writes only replica r).
+void pull_shard(const VarRecord& rec, std::size_t r);
 
 enum class PoolLifecycle : int { Idle = 0, InPhase = 1, ShutDown = 2 };
 

@@ -83,17 +83,19 @@ void* weight_shadow(const ReplicatedVariable& pvar, const std::shared_ptr<detail
     if (const char* e = std::getenv("SYNK_MLP_SHADOW"); e && e[0] == '0') return nullptr;  // A/B and tests
     if (r >= rec.shadows.size() || r >= rec.replicas.size() || rec.replicas[r].data() != params.data()) return nullptr;
     detail::VarRecord::Bf16Shadow& sh = rec.shadows[r];
-    if (sh.dims != dims || !sh.buf.has_storage() || sh.buf.owner().get() != rd.get()) {
+    if (sh.dims != dims || !sh.buf[0].has_storage() || sh.buf[0].owner().get() != rd.get()) {
         synk_bf16_shadow layout{};
         if (synk_mlp_bf16_shadow(dims.data(), static_cast<std::uint32_t>(dims.size() - 1), &layout) != SYNK_OK)
             return nullptr;  // more layers than the shadow supports: the casts go to the workspace
-        sh.buf = DevBuffer::alloc(rd, {(layout.bytes + 7) / 8}, DType::Float64);  // bytes; dtype is bookkeeping
+        for (DevBuffer& b : sh.buf)
+            b = DevBuffer::alloc(rd, {(layout.bytes + 7) / 8}, DType::Float64);  // bytes; dtype is bookkeeping
+        sh.cur = 0;
         sh.layout = layout;
         sh.dims = dims;
         sh.epoch = ~std::uint64_t(0);
     }
     *valid = sh.epoch == rec.epoch.load() && sh.params == params.data();
-    return sh.buf.data();
+    return sh.buf[sh.cur].data();
 }
 
 void mark_shadow_current(const ReplicatedVariable& pvar, std::size_t rank, const DevBuffer& params) {
@@ -133,6 +135,7 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     }
     const bool shadowed = pvar && compute == MlpCompute::Bf16TensorCore;
     if (shadowed) opts.shadow = weight_shadow(*pvar, rd, params, c.dims, &opts.shadow_valid);
+    opts.shadow_spare = opts.shadow != nullptr;  // a trainer update writes buf[cur ^ 1]
     int signalled = 0;
     detail::check(synk_mlp_loss_grad_opts(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(),
                                           xd.data(), yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws,

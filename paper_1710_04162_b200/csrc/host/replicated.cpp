@@ -35,6 +35,50 @@ VarRecord& record_of(const ReplicatedVariable& var) {
     return *var.rec_;
 }
 
+namespace {
+// Copy the chunks replica t lacks (every chunk q != t of every segment) from
+// their owners into dst on rd's stream.
+void pull_chunks(const VarRecord::Shard& sh, std::size_t t, DevBuffer& dst, const std::shared_ptr<RankDevice>& rd) {
+    const std::size_t W = sh.src.size();
+    const std::size_t es = dtype_size(dst.dtype());
+    for (auto [first, count] : sh.segs)
+        for (std::size_t q = 0; q < W; ++q) {
+            if (q == t) continue;
+            std::uint64_t lo = 0, hi = 0;
+            check(synk_chunk_range(count, static_cast<int>(W), static_cast<int>(q), &lo, &hi), "shard chunk");
+            if (lo >= hi) continue;
+            const std::size_t off = (first + lo) * es;
+            check(synk_copy(rd->h, static_cast<char*>(dst.data()) + off, static_cast<const char*>(sh.src[q].data()) + off,
+                            (hi - lo) * es),
+                  "gradient all-gather");
+        }
+}
+
+bool needs_pull(const VarRecord::Shard& sh, const DevBuffer& replica, std::size_t t) {
+    return t < sh.src.size() && replica.has_storage() && replica.data() == sh.src[t].data();
+}
+} // namespace
+
+void materialize(VarRecord& rec) {
+    if (!rec.shard) return;
+    VarRecord::Shard sh = std::move(*rec.shard);
+    rec.shard.reset();
+    std::vector<std::shared_ptr<RankDevice>> touched;
+    for (std::size_t t = 0; t < rec.replicas.size(); ++t) {
+        if (!needs_pull(sh, rec.replicas[t], t)) continue;
+        const auto& rd = rec.replicas[t].owner();
+        pull_chunks(sh, t, rec.replicas[t], rd);
+        touched.push_back(rd);
+    }
+    for (const auto& rd : touched) dev_sync(rd);
+}
+
+void pull_shard(const VarRecord& rec, std::size_t r) {
+    if (!rec.shard || r >= rec.replicas.size() || !needs_pull(*rec.shard, rec.replicas[r], r)) return;
+    DevBuffer dst = rec.replicas[r];  // shares the replica's storage
+    pull_chunks(*rec.shard, r, dst, dst.owner());
+}
+
 } // namespace detail
 
 namespace {
@@ -44,6 +88,16 @@ std::atomic<std::uint64_t> g_next_var{1};
 detail::VarRecord& live(const std::shared_ptr<detail::VarRecord>& rec, const char* what) {
     if (!rec) throw ArgumentError(std::string(what) + ": empty replicated-variable handle");
     return *rec;
+}
+
+// live() for the methods that read replica contents: a deferred gradient
+// all-gather is completed first (outside a phase only; in a phase the
+// lifecycle checks below raise before anything is read).
+detail::VarRecord& live_full(const std::shared_ptr<detail::VarRecord>& rec, const char* what) {
+    detail::VarRecord& r = live(rec, what);
+    if (r.shard && static_cast<detail::PoolLifecycle>(r.pool->lifecycle.load()) != detail::PoolLifecycle::InPhase)
+        detail::materialize(r);
+    return r;
 }
 
 void check_rank(const detail::VarRecord& rec, std::size_t rank, const char* what) {
@@ -124,7 +178,7 @@ std::size_t ReplicatedVariable::world() const { return live(rec_, "world").repli
 DType ReplicatedVariable::dtype() const { return live(rec_, "dtype").replicas.at(0).dtype(); }
 
 void ReplicatedVariable::broadcast(std::size_t src) {
-    detail::VarRecord& rec = live(rec_, "broadcast");
+    detail::VarRecord& rec = live_full(rec_, "broadcast");
     rec.mutated();
     check_rank(rec, src, "broadcast");
     detail::PoolState& st = *rec.pool;
@@ -168,7 +222,7 @@ void ReplicatedVariable::broadcast(std::size_t src) {
 }
 
 void ReplicatedVariable::all_reduce(ReduceOp op) {
-    detail::VarRecord& rec = live(rec_, "all_reduce");
+    detail::VarRecord& rec = live_full(rec_, "all_reduce");
     rec.mutated();
     not_gather(op, "all_reduce");
     check_same_shapes(rec, "all_reduce");
@@ -207,7 +261,7 @@ void ReplicatedVariable::all_reduce(ReduceOp op) {
 }
 
 void ReplicatedVariable::reduce(ReduceOp op, std::size_t dst) {
-    detail::VarRecord& rec = live(rec_, "reduce");
+    detail::VarRecord& rec = live_full(rec_, "reduce");
     rec.mutated();
     not_gather(op, "reduce");
     check_rank(rec, dst, "reduce");
@@ -230,7 +284,7 @@ void ReplicatedVariable::reduce(ReduceOp op, std::size_t dst) {
 }
 
 NdBuffer ReplicatedVariable::gather() const {
-    detail::VarRecord& rec = live(rec_, "gather");
+    detail::VarRecord& rec = live_full(rec_, "gather");
     detail::PoolState& st = *rec.pool;
     // concat_rows validation (tensor.cpp:287-313) happens on rank 0 inside
     // the phase in the reference, so its errors surface as PhaseError.
@@ -279,7 +333,7 @@ NdBuffer ReplicatedVariable::gather() const {
 }
 
 NdBuffer ReplicatedVariable::get_value(std::size_t rank) const {
-    detail::VarRecord& rec = live(rec_, "get_value");
+    detail::VarRecord& rec = live_full(rec_, "get_value");
     check_rank(rec, rank, "get_value");
     no_phase(rec, "get_value");
     return detail::dev_to_host(rec.replicas[rank]);
@@ -299,6 +353,7 @@ void ReplicatedVariable::set_value(std::size_t rank, const NdBuffer& value) {
 void ReplicatedVariable::scatter_value(const NdBuffer& data, const std::optional<IndexSelection>& indexes) {
     detail::VarRecord& rec = live(rec_, "scatter_value");
     rec.mutated();
+    rec.shard.reset();  // every replica is replaced
     const std::size_t n = data.rows();
     std::size_t eff = n;
     if (indexes) {
@@ -322,6 +377,7 @@ void ReplicatedVariable::scatter_value(const SharedInputArray& data, const std::
 void ReplicatedVariable::scatter_uniform(const std::vector<std::size_t>& shape, DType dtype, std::uint64_t seed) {
     detail::VarRecord& rec = live(rec_, "scatter_uniform");
     rec.mutated();
+    rec.shard.reset();  // every replica is replaced
     if (shape.empty()) throw ShapeError("scatter_uniform: a rank-0 shape has no rows to scatter");
     const std::size_t row = element_count(shape) / std::max<std::size_t>(shape[0], 1);
     std::vector<RowRange> parts = partition_rows(shape[0], rec.replicas.size());
@@ -340,7 +396,7 @@ void ReplicatedVariable::scatter_uniform(const std::vector<std::size_t>& shape, 
 }
 
 bool ReplicatedVariable::replicas_coherent() const {
-    detail::VarRecord& rec = live(rec_, "replicas_coherent");
+    detail::VarRecord& rec = live_full(rec_, "replicas_coherent");
     no_phase(rec, "replicas_coherent");
     const DevBuffer& a = rec.replicas[0];
     for (std::size_t r = 1; r < rec.replicas.size(); ++r) {
@@ -354,7 +410,7 @@ bool ReplicatedVariable::replicas_coherent() const {
 }
 
 DevBuffer ReplicatedVariable::device_value(std::size_t rank) const {
-    detail::VarRecord& rec = live(rec_, "device_value");
+    detail::VarRecord& rec = live_full(rec_, "device_value");
     rec.mutated();
     check_rank(rec, rank, "device_value");
     return rec.replicas[rank];

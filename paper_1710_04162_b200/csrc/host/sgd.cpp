@@ -269,6 +269,12 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     std::vector<char> seg_cover(W, 0);
     std::vector<char> shadow_written(W, 0);
     const std::size_t n_total = grads[0].size();
+    // Deferred all-gather of the reduced gradient (SYNK_STEP_GRADS_LOCAL):
+    // each rank keeps its own chunk of every segment; readers of `grads`
+    // complete the replicas (VarRecord::shard). Segments as rank 0 ran them.
+    const bool defer = W > 1 && !st->nccl;
+    const int step_flags = defer ? SYNK_STEP_GRADS_LOCAL : 0;
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> shard_segs;
 
     auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows, const std::vector<GradSegment>& segs) {
         const auto& rd = st->ranks[r];
@@ -329,9 +335,9 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             bool ok = W <= SYNK_SHADOW_MAX_WORLD && prec.shadows.size() == W && dt == SYNK_F32;
             for (std::size_t p = 0; p < W && ok; ++p) {
                 const detail::VarRecord::Bf16Shadow& sh = prec.shadows[p];
-                ok = sh.buf.has_storage() && sh.params == pp[p] && sh.epoch == prec.epoch.load() &&
-                     sh.dims == prec.shadows[0].dims;
-                shb[p] = ok ? sh.buf.data() : nullptr;
+                ok = sh.buf[0].has_storage() && sh.buf[1].has_storage() && sh.params == pp[p] &&
+                     sh.epoch == prec.epoch.load() && sh.dims == prec.shadows[0].dims;
+                shb[p] = ok ? sh.buf[sh.cur ^ 1].data() : nullptr;  // the spare: the kernel reads buf[cur]
             }
             if (ok) shl = &prec.shadows[0].layout;
             shadow_written[r] = ok;
@@ -348,10 +354,12 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             // W = 1: the update directly follows the compute end (event 3) on this stream
             if (r == 0 && t0_timer && W > 1) detail::check(synk_timer_record(rd->h, t0_timer, 4), "timer");
             if (r == 0) update_from_compute_end_ = W == 1;
+            if (r == 0) shard_segs.assign(1, {0, grads[r].size()});
             detail::check(synk_all_reduce_step_ex(rd->h, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                   hyper.data(), lr_, t_next, pp.data(), gp.data(),
                                                   a0.empty() ? nullptr : a0.data(), a1.empty() ? nullptr : a1.data(),
-                                                  grads[r].size(), coherent ? 1 : 0, 0, shl, shb.data()),
+                                                  grads[r].size(), (coherent ? SYNK_STEP_COHERENT : 0) | step_flags, 0,
+                                                  shl, shb.data()),
                           "fused all-reduce + update");
             if (r == 0 && timing) detail::check(synk_mark(rd->h, &mb), "mark");
             if (r == 0 && t0_timer) detail::check(synk_timer_record(rd->h, t0_timer, 5), "timer");
@@ -376,10 +384,12 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             if (r == 0 && t0_timer && k == 0) detail::check(synk_timer_record(aux, t0_timer, 4), "timer");
             if (r == 0 && k == 0) update_from_compute_end_ = false;
             std::vector<void*> ps = at(pp, g.first), gs = at(gp, g.first), x0 = at(a0, g.first), x1 = at(a1, g.first);
+            if (r == 0) shard_segs.emplace_back(g.first, g.count);
             detail::check(synk_all_reduce_step_ex(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                   hyper.data(), lr_, t_next, ps.data(), gs.data(),
                                                   a0.empty() ? nullptr : x0.data(), a1.empty() ? nullptr : x1.data(),
-                                                  g.count, coherent ? 1 : 0, g.first, shl, shb.data()),
+                                                  g.count, (coherent ? SYNK_STEP_COHERENT : 0) | step_flags, g.first,
+                                                  shl, shb.data()),
                           "segment all-reduce + update");
         }
         if (r == 0 && timing) detail::check(synk_mark(aux, &mb), "mark");
@@ -403,15 +413,20 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
         rep.step_call.total_s = sec;
     }
     rep.step_call.rank_rows.assign(W, 1);
-    detail::record_of(block_.grads).coherent = true;
-    detail::record_of(block_.grads).mutated();
+    detail::VarRecord& grec = detail::record_of(block_.grads);
+    grec.coherent = true;  // logically: every reader completes the replicas first
+    grec.mutated();
+    if (defer && !shard_segs.empty()) grec.shard = detail::VarRecord::Shard{grads, shard_segs};
     detail::VarRecord& prec = detail::record_of(block_.params);
     prec.coherent = true;
     prec.mutated();
     bool all_shadows = true;
     for (std::size_t r = 0; r < W; ++r) all_shadows = all_shadows && shadow_written[r];
-    if (all_shadows)  // the update wrote every rank's shadow with the new params
-        for (auto& sh : prec.shadows) sh.epoch = prec.epoch.load();
+    if (all_shadows)  // the update wrote every rank's spare shadow with the new params
+        for (auto& sh : prec.shadows) {
+            sh.cur ^= 1;
+            sh.epoch = prec.epoch.load();
+        }
     for (const ReplicatedVariable& a : aux_) {
         detail::record_of(a).coherent = true;
         detail::record_of(a).mutated();

@@ -135,3 +135,45 @@ def test_bf16_weight_shadow_bitwise_and_invalidation(sk, world):
     assert runs["1"][0] == runs["0"][0]
     assert runs["1"][1] == runs["0"][1]
     assert runs["1"][2] == runs["0"][2]
+
+
+@pytest.mark.parametrize("world,compute,batches", [
+    (2, "native", [256, 256]),
+    (3, "bf16", [768, 768]),
+    (3, "bf16", [768, 2, 768, 2]),   # 2-row batches: rank 2 gets no rows (no update, pulls its chunks)
+    (4, "native", [512, 3]),
+])
+def test_deferred_gradient_all_gather(sk, world, compute, batches):
+    """The fused step leaves the reduced gradient sharded (rank r keeps chunk
+    r of every segment, SYNK_STEP_GRADS_LOCAL): every reader -- get(r), a
+    kernel taking the gradients as a broadcast input, all_reduce, coherent --
+    and the next step's zero-row ranks must see exactly what the two-phase
+    step (check_finite=True, which writes every replica) leaves, bit for bit."""
+    cfg = sk.MlpConfig(in_dim=96, width=256, out_dim=100, layers=3, seed=11)
+    x, y = sk.mlp_make_dataset(1024, cfg, seed=12, dtype="f32")
+    seen = {}
+    for two_phase in (False, True):
+        with sk.Pool(workers=world) as pool:
+            block = sk.ParamBlock.create(pool, sk.mlp_init_params(cfg, "f32"))
+            f = sk.mlp_grad_function(pool, block, compute=compute)
+            ident = sk.make_function(pool, sk.identity_kernel(), ["broadcast"], ["gather"])
+            sk.distribute(pool)
+            tr = sk.Trainer(pool, block, sk.MomentumRule(), lr=1e-2, check_finite=two_phase)
+            rng = np.random.default_rng(3)
+            out = []
+            for k, b in enumerate(batches):
+                tr.train_step(f, [x, y], indexes=rng.integers(0, x.shape[0], b))
+                if k == 0:  # a kernel reading the gradients right after a step
+                    (cat,) = ident.call([block.grads])
+                    out.append(cat)
+            out += [block.grads.get(r) for r in range(world)]
+            out.append(block.params.get(world - 1))
+            assert block.grads.coherent and block.params.coherent
+            block.grads.all_reduce("max")
+            out.append(block.grads.get(0))
+            seen[two_phase] = out
+    for a, b in zip(seen[False], seen[True]):
+        assert a.tobytes() == b.tobytes()
+    cat = seen[False][0].reshape(world, -1)  # every rank's replica, as the kernel saw it
+    assert all(cat[r].tobytes() == cat[0].tobytes() for r in range(world))
+    assert cat.shape[1] == sum(p.size for p in sk.mlp_init_params(cfg, "f32"))

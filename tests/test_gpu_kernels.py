@@ -347,10 +347,13 @@ def test_optimizer_step_bit_exact(oracle, rule, dtype):
 
 
 @pytest.mark.parametrize("rule", ["sgd", "adam"])
-@pytest.mark.parametrize("coherent", [True, False])
-def test_fused_all_reduce_step_bit_exact(oracle, rule, coherent):
+@pytest.mark.parametrize("coherent,grads_local", [(True, False), (False, False), (True, True)])
+def test_fused_all_reduce_step_bit_exact(oracle, rule, coherent, grads_local):
     """Gradient tree all-reduce (mean) + update in one kernel per rank =
-    reference all_reduce(Mean) followed by the per-rank step."""
+    reference all_reduce(Mean) followed by the per-rank step. With
+    SYNK_STEP_GRADS_LOCAL (deferred all-gather) rank r writes the reduced
+    gradient into its own replica's chunk only; every other byte of the
+    gradient replicas is left as it was."""
     rng = np.random.default_rng(9)
     world, n = 4, 40961
     naux = 2 if rule == "adam" else 0
@@ -369,13 +372,21 @@ def test_fused_all_reduce_step_bit_exact(oracle, rule, coherent):
         for r in range(world):
             check(lib().synk_all_reduce_step(R[r], world, F32, OPS["mean"], RULES[rule], hyper.ctypes.data_as(_vp),
                                              ctypes.c_double(0.01), _u64(1), P, G, a0, a1, _u64(n),
-                                             1 if coherent else 0), "fused")
+                                             (1 if coherent else 0) | (2 if grads_local else 0)), "fused")
         for r in range(world):
             check(R.sync(r), "sync")
         g_ref = oracle.tree_fold(grads, "mean")
         for r in range(world):
             p_ref, aux_ref = _oracle_step(oracle, rule, params[r], g_ref, aux[r], 0.01, 1)
-            assert R.download(dg[r], (n,), np.float32, r).tobytes() == g_ref.tobytes()
+            got = R.download(dg[r], (n,), np.float32, r)
+            if grads_local:
+                lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+                check(lib().synk_chunk_range(_u64(n), world, r, ctypes.byref(lo), ctypes.byref(hi)), "chunk")
+                want = grads[r].copy()
+                want[lo.value:hi.value] = g_ref[lo.value:hi.value]
+                assert got.tobytes() == want.tobytes()
+            else:
+                assert got.tobytes() == g_ref.tobytes()
             assert R.download(dp[r], (n,), np.float32, r).tobytes() == p_ref.tobytes()
             for k in range(naux):
                 assert R.download(da[k][r], (n,), np.float32, r).tobytes() == aux_ref[k].tobytes()
