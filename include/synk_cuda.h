@@ -250,6 +250,9 @@ int synk_optimizer_step(synk_dev* dev, int dtype, int rule, const double* hyper,
  * 2(W-1)/W * S instead of 3(W-1)/W * S). */
 #define SYNK_STEP_COHERENT 1
 #define SYNK_STEP_GRADS_LOCAL 2
+/* SYNK_STEP_BACKGROUND: the launch overlaps other work on another stream of
+ * the same GPU (the bucketed update beside the backward GEMMs): a small grid. */
+#define SYNK_STEP_BACKGROUND 4
 int synk_all_reduce_step(synk_dev* dev, int world, int dtype, int grad_op, int rule,
                          const double* hyper, double lr, uint64_t t, void* const* params,
                          void* const* grads, void* const* aux0, void* const* aux1, uint64_t n,

@@ -491,6 +491,17 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     const int vec_bytes = aligned(32) && forced != 16 ? 32 : (aligned(16) ? 16 : 0);
     const uint64_t items = vec_bytes ? (hi - lo) / (vec_bytes / sizeof(T)) + 1 : hi - lo;
     unsigned grid = synk::grid_for(d, items, kBlock);
+    if (flags & SYNK_STEP_BACKGROUND) {
+        // Overlapped with tensor-core GEMMs on the other stream: a few CTAs
+        // stream the segment at a fraction of HBM bandwidth instead of
+        // competing for every SM's issue slots with the persistent GEMM.
+        static const unsigned bg = [] {
+            const char* e = getenv("SYNK_BG_CTAS");  // A/B: CTAs of a background update
+            const int v = e ? atoi(e) : 0;
+            return v > 0 ? (unsigned)v : 32u;
+        }();
+        grid = std::min(grid, bg);
+    }
     Shadow none{};
     const Shadow& S = sh ? *sh : none;
     const bool with = sh != nullptr;

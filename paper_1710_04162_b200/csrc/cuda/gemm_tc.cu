@@ -201,6 +201,20 @@ struct ActPrefetch {
     }
 };
 
+// 256-bit global accesses (sm_100 ld/st .v8.b32): one instruction per
+// 32-byte sector per lane. The epilogue's lanes own different rows, so a
+// 16-byte access leaves every sector of the warp's request half used.
+__device__ __forceinline__ void ld256_stream(const void* p, uint4& lo, uint4& hi) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(void* p, const uint32_t (&w)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+
 // Split-K fold through distributed shared memory (cluster = the S split CTAs
 // of one output tile, cluster rank = blockIdx.z): every CTA parks its fp32
 // partial tile in its own (now idle) operand ring, the cluster syncs, CTA z
@@ -714,17 +728,77 @@ __global__ void __launch_bounds__(PThreads, 1)
         const bool vec_c = epi.c && ((epi.ldc * es) % 16 == 0) && ((reinterpret_cast<uintptr_t>(epi.c) & 15) == 0);
         const bool vec_act = epi.mode == EPI_TANH_GRAD && ((epi.ldact * es) % 16 == 0) &&
                              ((reinterpret_cast<uintptr_t>(epi.act) & 15) == 0);
+        const bool pre_ok = epi.mode == EPI_TANH_GRAD && epi.out_bf16 && vec_act;
+        // 32-byte alignment of every 16-column chunk (bf16: 32 B) for the 256-bit paths
+        const bool act32 = pre_ok && (epi.ldact * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(epi.act) & 31) == 0;
+        const bool c32 = pre_ok && epi.c && (epi.ldc * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(epi.c) & 31) == 0;
         uint32_t tl = 0;
         for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl & 1;
             const uint64_t m0 = (t / num_n) * BM, n0 = (uint64_t)(t % num_n) * PBN;
-            mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
-            tc_fence_after();
             const uint64_t m = m0 + quad * 32 + lane;
             const uint32_t base = tmem + acc * PBN + ((uint32_t)(quad * 32) << 16);
             const int cbeg = half * (PBN / 2), cend = cbeg + PBN / 2;
-            ActPrefetch pf{epi.mode == EPI_TANH_GRAD && epi.out_bf16 && vec_act && m < M,
-                           static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact, {}};
+            if (pre_ok && n0 + cend <= N) {  // warp-uniform: tcgen05.ld is .sync.aligned
+                // tanh-derivative epilogue, whole half-row inside the matrix:
+                // the thread's 128 activations (256 B, 16 loads) are issued
+                // BEFORE waiting for the accumulator, so their HBM latency
+                // hides behind this tile's MMAs -- 64 KB in flight per SM
+                // instead of one 32-byte chunk per thread (the short-K dX
+                // products are bound by this read, not by the tensor cores).
+                const uint4* src =
+                    reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact + n0 + cbeg);
+                const bool row = m < M;
+                uint4 a[16];
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    if (row && act32) {
+                        ld256_stream(src + i, a[i], a[i + 1]);
+                    } else {
+                        a[i] = row ? __ldcs(src + i) : make_uint4(0, 0, 0, 0);
+                        a[i + 1] = row ? __ldcs(src + i + 1) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+                mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    uint32_t r[16];
+                    tmem_ld16(base + cbeg + 16 * k, r);
+                    if (!row) continue;
+                    if (c32) {  // the 16 bf16 results of the chunk as one 32-byte store
+                        float v[16];
+                        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&a[2 * k]);
+                        uint32_t w[8];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float x = __bfloat162float(h[j]);
+                            v[j] = __uint_as_float(r[j]) * (1.0f - x * x);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                            w[j] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                        st256(static_cast<__nv_bfloat16*>(epi.c) + m * epi.ldc + n0 + cbeg + 16 * k, w);
+                        if (epi.ct) {
+                            __nv_bfloat16* col = static_cast<__nv_bfloat16*>(epi.ct) + (n0 + cbeg + 16 * k) * epi.ldct + m;
+                            const __nv_bfloat16* hw = reinterpret_cast<const __nv_bfloat16*>(w);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j, col += epi.ldct) *col = hw[j];
+                        }
+                    } else {
+                        epi_chunk_fast<EPI_TANH_GRAD, true>(epi, m, n0 + cbeg + 16 * k, r, vec_c, true, false, true,
+                                                            a[2 * k], a[2 * k + 1]);
+                    }
+                }
+                tc_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+                continue;
+            }
+            mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
+            tc_fence_after();
+            ActPrefetch pf{pre_ok && m < M, static_cast<const __nv_bfloat16*>(epi.act) + m * epi.ldact, {}};
             if (pf.on && n0 + cbeg + 16 <= N) pf.load(n0 + cbeg);
 #pragma unroll 1
             for (int c0 = cbeg; c0 < cend; c0 += 16) {

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 
 #include "internal.hpp"
@@ -274,6 +275,15 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
     // complete the replicas (VarRecord::shard). Segments as rank 0 ran them.
     const bool defer = W > 1 && !st->nccl;
     const int step_flags = defer ? SYNK_STEP_GRADS_LOCAL : 0;
+    // Segment updates other than the last overlap the remaining backward
+    // GEMMs. SYNK_BG_UPDATES=1 runs them as small grids (SYNK_BG_CTAS): the
+    // GEMMs lose less (dX1 + gW0 -45 us) but the update then takes 4-15x
+    // longer and the step is slower (1.27-2.1 vs 1.12 ms,
+    // profiles/r02_c5_step.md), so full grids are the default.
+    static const bool bg_updates = [] {
+        const char* e = std::getenv("SYNK_BG_UPDATES");
+        return e && e[0] == '1';
+    }();
     std::vector<std::pair<std::uint64_t, std::uint64_t>> shard_segs;
 
     auto tail = [&](std::size_t r, const std::vector<std::size_t>& rows, const std::vector<GradSegment>& segs) {
@@ -388,7 +398,10 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             detail::check(synk_all_reduce_step_ex(aux, static_cast<int>(W), dt, detail::synk_op(opts_.grad_op), code,
                                                   hyper.data(), lr_, t_next, ps.data(), gs.data(),
                                                   a0.empty() ? nullptr : x0.data(), a1.empty() ? nullptr : x1.data(),
-                                                  g.count, (coherent ? SYNK_STEP_COHERENT : 0) | step_flags, g.first,
+                                                  g.count,
+                                                  (coherent ? SYNK_STEP_COHERENT : 0) | step_flags |
+                                                      (k + 1 < segs.size() && bg_updates ? SYNK_STEP_BACKGROUND : 0),
+                                                  g.first,
                                                   shl, shb.data()),
                           "segment all-reduce + update");
         }
