@@ -495,7 +495,7 @@ def gather_headline(args, n_gpus, devices, dist, world):
 
 SGD_MODELS = {
     "c1": {"dims": [784, 512, 10], "per_gpu": 256, "rows": 65536, "compute": "native", "warm": 30, "dtype": "f32",
-           "label": "C1: MLP 784-512-10 fp32 (FFMA/DFMA GEMMs), indexed from a 65536-row SharedInput (HBM mirror), "
+           "label": "C1: MLP 784-512-10 fp32 (tcgen05 3xTF32 GEMMs at fp32 accuracy), indexed from a 65536-row SharedInput (HBM mirror), "
                     "SGD lr 0.01, gradient all-reduce mean fused with the update"},
     "c5": {"dims": [2048, 4096, 4096, 100], "per_gpu": 8192, "rows": 16384, "compute": "bf16", "warm": 3,
            "dtype": "bf16",

@@ -297,6 +297,51 @@ int synk_gemm_tc(synk_dev* dev, int kind, uint64_t M, uint64_t N, uint64_t K, co
  * The tensor cores read MN-major shared-memory tiles directly (UMMA major
  * bits), so the MLP's weight/activation/delta transposes (mlp.cpp:31-73,
  * 169-208 use W^T, a^T, delta^T) are never materialised. */
+/* fp32-accurate tensor-core GEMM (3xTF32) for the f32 example function
+ * (replaces mlp.cpp:31-73's f32 products): C[M x N] = epilogue(A . B^T) with A
+ * [M x K], B [N x K] K-major fp32 given as tf32 hi/lo parts (synk_tf32_split;
+ * leading dims lda/ldb in elements, rows 16-byte aligned). Each 32-element K
+ * block is accumulated on tcgen05 (kind::tf32: hi.lo + lo.hi + hi.hi) into a
+ * fresh TMEM accumulator and added into fp32 registers (round-to-nearest);
+ * split-K partials (shape-fixed, <= 8) are folded in f64 in rank order. Any
+ * subset of outputs: c (fp32 row-major, ldc); c_hi/c_lo (the result's tf32
+ * split, row-major, ldh); ct_hi/ct_lo (transposed split, [n][m], ldt). act
+ * (EPI_TANH_GRAD) is fp32 [M x N] with leading dim ldact. */
+int synk_gemm_f32x3(synk_dev* dev, uint64_t M, uint64_t N, uint64_t K, const float* a_hi, const float* a_lo,
+                    uint64_t lda, const float* b_hi, const float* b_lo, uint64_t ldb, int epilogue, float* c,
+                    uint64_t ldc, const float* bias, const float* act, uint64_t ldact, float* c_hi, float* c_lo,
+                    uint64_t ldh, float* ct_hi, float* ct_lo, uint64_t ldt);
+/* tf32 split of in (rows x cols, ld_in; row r is in row rowmap[r] when rowmap
+ * != NULL, u64 in HBM): hi = rna_tf32(x), lo = rna_tf32(x - hi), row-major
+ * (hi/lo, ld_o) and/or transposed (hi_t/lo_t, cols x rows, ld_t). */
+int synk_tf32_split(synk_dev* dev, const float* in, const uint64_t* rowmap, uint64_t rows, uint64_t cols,
+                    uint64_t ld_in, float* hi, float* lo, uint64_t ld_o, float* hi_t, float* lo_t, uint64_t ld_t);
+/* Sets up to 64 split rows to (value, 0): the constant ones row under a^T that
+ * turns the weight-gradient product into [gW; gb] (mlp.cpp:193-203). */
+#define SYNK_TF32_MAX_ROWS 64
+typedef struct synk_tf32_rows {
+    float* hi[SYNK_TF32_MAX_ROWS];
+    float* lo[SYNK_TF32_MAX_ROWS];
+    uint64_t len[SYNK_TF32_MAX_ROWS];
+    uint32_t count;
+    float value;
+} synk_tf32_rows;
+int synk_tf32_fill_rows(synk_dev* dev, const synk_tf32_rows* rows);
+/* A step's whole operand staging in one launch: up to 16 split jobs (each as
+ * synk_tf32_split) plus the constant rows (fill may be NULL). */
+#define SYNK_TF32_MAX_JOBS 16
+typedef struct synk_tf32_job {
+    const float* in;
+    const uint64_t* rowmap;
+    uint64_t rows, cols, ld_in;
+    float* hi;
+    float* lo;
+    uint64_t ld_o;
+    float* hi_t;
+    float* lo_t;
+    uint64_t ld_t;
+} synk_tf32_job;
+int synk_tf32_stage(synk_dev* dev, const synk_tf32_job* jobs, uint32_t count, const synk_tf32_rows* fill);
 /* bf16 weight shadow: a per-rank HBM copy of an MLP's weight matrices in the
  * bf16 operand layout of the tensor-core path (W_l row-major with padded
  * leading dimension, plus W_l^T for narrow layers). The fused update writes
@@ -398,6 +443,10 @@ int synk_mlp_loss_grad_opts(synk_dev* dev, int dtype, int compute, const uint64_
  * with bf16 operands and fp32 accumulation (the wide-MLP config). */
 #define SYNK_MLP_NATIVE 0
 #define SYNK_MLP_BF16_TC 1
+/* f32 parameters, every product on the tensor cores at fp32 accuracy
+ * (synk_gemm_f32x3). SYNK_MLP_NATIVE with f32 parameters runs this path too
+ * unless SYNK_MLP_F32=ffma (CUDA-core FFMA products, A/B runs). */
+#define SYNK_MLP_F32_TC 2
 int synk_mlp_workspace_bytes_ex(int dtype, int compute, const uint64_t* dims, uint32_t layers, uint64_t n,
                                 uint64_t* bytes);
 int synk_mlp_loss_grad_ex(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,

@@ -8,8 +8,12 @@
 // Each dense product is one tiled GEMM launch with the elementwise work fused
 // into its epilogue (bias+tanh, bias, tanh-derivative); the loss/delta pass
 // and the bias-gradient column sums are deterministic block reductions.
-// This file holds the SIMT path (FFMA for f32, DFMA for f64 — the f64 path
-// is what the reference's f64 trajectories are checked against at 1e-10).
+// Paths: f32 parameters run every product on the tensor cores at fp32
+// accuracy (3xTF32, gemm_f32x3.cu: loss_grad_f32tc below, the default);
+// f64 runs the SIMT DFMA products (what the reference's f64 trajectories are
+// checked against at 1e-10), and the same SIMT kernel in f32 (FFMA) is kept
+// as the A/B baseline (SYNK_MLP_F32=ffma); the wide bf16 MLP (config C5)
+// runs loss_grad_bf16 on gemm_tc.cu.
 
 #include <cstdio>
 #include <cuda_bf16.h>
@@ -17,6 +21,7 @@
 
 #include <algorithm>
 #include <stdlib.h>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -191,6 +196,18 @@ uint64_t splitk_elems(int es, const uint64_t* dims, uint32_t layers, uint64_t n)
     return best;
 }
 
+// tf32 hi/lo split of delta, row-major (hi/lo, ld_o; may be null) and
+// transposed (hi_t/lo_t, ld_t): written by the loss kernel for the f32
+// tensor-core path (gemm_f32x3.cu operands).
+struct DeltaSplit {
+    float* hi = nullptr;
+    float* lo = nullptr;
+    uint64_t ld_o = 0;
+    float* hi_t = nullptr;
+    float* lo_t = nullptr;
+    uint64_t ld_t = 0;
+};
+
 // delta = (pred - y) * inv_n ; per-CTA partial of sum (pred - y)^2 in f64.
 // With `counter`, the last CTA to finish also folds the per-CTA partials in a
 // fixed order (thread t sums partials t, t+256, ..., then a fixed shared-memory
@@ -203,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
                                                               unsigned* __restrict__ counter = nullptr,
                                                               double scale = 0.0, double* __restrict__ loss = nullptr,
                                                               const uint64_t* __restrict__ yrows = nullptr,
-                                                              uint64_t ycols = 1) {
+                                                              uint64_t ycols = 1, DeltaSplit ds = {}) {
     __shared__ double red[kThreads];
     __shared__ int last;
     double s = 0.0;
@@ -213,6 +230,17 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
         double diff = __dsub_rn((double)pred[i], (double)y[yi]);
         s = __dadd_rn(s, __dmul_rn(diff, diff));
         delta[i] = (T)__dmul_rn(diff, inv_n);
+        if constexpr (sizeof(T) == 4) {
+            if (ds.hi_t) {  // the f32 tensor-core path's operand forms of delta
+                const float v = (float)__dmul_rn(diff, inv_n);
+                uint32_t h, l;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - __uint_as_float(h)));
+                const uint64_t m = i / ycols, c = i % ycols;
+                ds.hi_t[c * ds.ld_t + m] = __uint_as_float(h), ds.lo_t[c * ds.ld_t + m] = __uint_as_float(l);
+                if (ds.hi) ds.hi[m * ds.ld_o + c] = __uint_as_float(h), ds.lo[m * ds.ld_o + c] = __uint_as_float(l);
+            }
+        }
     }
     red[threadIdx.x] = s;
     __syncthreads();
@@ -352,6 +380,160 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
         }
     }
     return SYNK_OK;
+}
+
+// ---- f32 tensor-core path (config C1: fp32 accuracy on tcgen05, 3xTF32) ---------------
+// Every product is one synk_gemm_f32x3 launch (gemm_f32x3.cu): operands are
+// K-major tf32 hi/lo pairs, and each producer emits its result directly in the
+// form its consumers read, so the only separate staging launches are the
+// input batch (gathered through the index list in the same pass), the weights
+// and the loss delta:
+//   forward   a_{l+1} = tanh(a_l . W_l + b_l): A = a_l split, B = W_l^T split;
+//             the epilogue writes a_{l+1} (f32, for tanh'), its split and
+//             its transposed split (the weight gradient's A)
+//   gradient  [gW_l; gb_l] = [a_l^T; 1] . delta: A = a_l^T split whose extra
+//             row is the constant 1.0 (hi) / 0 (lo), B = delta^T split
+//   dX        delta_prev = (delta . W_l^T) * (1 - a_l^2): A = delta split,
+//             B = W_l split; the epilogue writes delta_prev's split and
+//             transposed split
+// Same layer algebra and loss/delta kernel as loss_grad_t (mlp.cpp:134-218).
+
+inline uint64_t pad4(uint64_t v) { return (v + 3) / 4 * 4; }
+
+struct TcPlan {
+    uint64_t n, L;
+    uint64_t act[65];             // f32 a_l (l = 1..L), n x d_l; a_L = prediction
+    uint64_t ah[64], al[64];      // a_l split, n x pad4(d_l)          (l = 0..L-1)
+    uint64_t ath[64], atl[64];    // a_l^T split, (d_l + 1) x pad4(n)  (row d_l = ones)
+    uint64_t wth[64], wtl[64];    // W_l^T split, d_{l+1} x pad4(d_l)
+    uint64_t wh[64], wl[64];      // W_l split, d_l x pad4(d_{l+1})      (l >= 1)
+    uint64_t dh[2], dl[2];        // delta split ping-pong, n x pad4(maxd)
+    uint64_t dth[2], dtl[2];      // delta^T split ping-pong, maxd x pad4(n)
+    uint64_t delta, partial, total;
+};
+
+TcPlan make_tc_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t maxd) {
+    TcPlan p{};
+    p.n = n;
+    p.L = L;
+    uint64_t at = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t o = at;
+        at += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    for (uint32_t l = 1; l <= L; ++l) p.act[l] = take(n * dims[l] * 4);
+    for (uint32_t l = 0; l < L; ++l) {
+        p.ah[l] = take(n * pad4(dims[l]) * 4);
+        p.al[l] = take(n * pad4(dims[l]) * 4);
+        p.ath[l] = take((dims[l] + 1) * pad4(n) * 4);
+        p.atl[l] = take((dims[l] + 1) * pad4(n) * 4);
+        p.wth[l] = take(dims[l + 1] * pad4(dims[l]) * 4);
+        p.wtl[l] = take(dims[l + 1] * pad4(dims[l]) * 4);
+        if (l >= 1) {
+            p.wh[l] = take(dims[l] * pad4(dims[l + 1]) * 4);
+            p.wl[l] = take(dims[l] * pad4(dims[l + 1]) * 4);
+        }
+    }
+    for (int b = 0; b < 2; ++b) {
+        p.dh[b] = take(n * pad4(maxd) * 4);
+        p.dl[b] = take(n * pad4(maxd) * 4);
+        p.dth[b] = take(maxd * pad4(n) * 4);
+        p.dtl[b] = take(maxd * pad4(n) * 4);
+    }
+    p.delta = take(n * dims[L] * 4);
+    p.partial = take(kLossBlocks * sizeof(double));
+    p.total = at;
+    return p;
+}
+
+int loss_grad_f32tc(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P, const float* theta, const float* x,
+                    const float* y, uint64_t n, double* loss, float* grad, void* ws, const uint64_t* rows) {
+    const TcPlan T = make_tc_plan(dims, L, n, P.maxd);
+    char* base = static_cast<char*>(ws);
+    auto F = [&](uint64_t off) { return reinterpret_cast<float*>(base + off); };
+    const uint64_t pn = pad4(n);
+
+    // one staging launch: the constant ones row under every a_l^T (bias
+    // gradient through the GEMM), the input batch (index-fused: row i is
+    // source row rows[i]) -> a_0 split + a_0^T split, and the weights: W_l^T
+    // split (forward B) and, below the first layer, W_l split (dX B)
+    synk_tf32_rows ones{};
+    for (uint32_t l = 0; l < L; ++l) {
+        ones.hi[l] = F(T.ath[l]) + dims[l] * pn;
+        ones.lo[l] = F(T.atl[l]) + dims[l] * pn;
+        ones.len[l] = n;
+    }
+    ones.count = L;
+    ones.value = 1.0f;
+    std::vector<synk_tf32_job> jobs;
+    jobs.push_back({x, rows, n, dims[0], dims[0], F(T.ah[0]), F(T.al[0]), pad4(dims[0]), F(T.ath[0]), F(T.atl[0]), pn});
+    for (uint32_t l = 0; l < L; ++l) {
+        const bool rows_too = l >= 1;
+        jobs.push_back({theta + P.woff[l], nullptr, dims[l], dims[l + 1], dims[l + 1], rows_too ? F(T.wh[l]) : nullptr,
+                        rows_too ? F(T.wl[l]) : nullptr, pad4(dims[l + 1]), F(T.wth[l]), F(T.wtl[l]), pad4(dims[l])});
+    }
+    for (size_t at = 0; at < jobs.size(); at += SYNK_TF32_MAX_JOBS) {
+        const uint32_t cnt = (uint32_t)std::min<size_t>(SYNK_TF32_MAX_JOBS, jobs.size() - at);
+        if (int rc = synk_tf32_stage(d, jobs.data() + at, cnt, at == 0 ? &ones : nullptr); rc) return rc;
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+        const bool hidden = l + 1 < L;
+        if (int rc = synk_gemm_f32x3(d, n, dims[l + 1], dims[l], F(T.ah[l]), F(T.al[l]), pad4(dims[l]), F(T.wth[l]),
+                                     F(T.wtl[l]), pad4(dims[l]), hidden ? SYNK_EPI_BIAS_TANH : SYNK_EPI_BIAS,
+                                     F(T.act[l + 1]), dims[l + 1], theta + P.boff[l], nullptr, 0,
+                                     hidden ? F(T.ah[l + 1]) : nullptr, hidden ? F(T.al[l + 1]) : nullptr,
+                                     pad4(dims[l + 1]), hidden ? F(T.ath[l + 1]) : nullptr,
+                                     hidden ? F(T.atl[l + 1]) : nullptr, pn);
+            rc)
+            return rc;
+    }
+    const uint64_t n_el = n * dims[L];
+    const int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
+    const double inv_n = 1.0 / (double)n;
+    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(F(T.act[L]), y, n_el, inv_n, F(T.delta),
+                                                                 reinterpret_cast<double*>(base + T.partial),
+                                                                 reinterpret_cast<unsigned*>(d->flags_dev + 3),
+                                                                 0.5 * inv_n, loss, rows, dims[L],
+                                                                 DeltaSplit{L >= 2 ? F(T.dh[0]) : nullptr,
+                                                                            L >= 2 ? F(T.dl[0]) : nullptr, pad4(dims[L]),
+                                                                            F(T.dth[0]), F(T.dtl[0]), pn});
+    SYNK_LAUNCHED("loss_delta_kernel");
+    int cur = 0;
+    for (uint32_t l = L; l-- > 0;) {
+        // [gW_l; gb_l]: M = d_l + 1 (row d_l of a_l^T is ones), lands on b_l after W_l
+        if (int rc = synk_gemm_f32x3(d, dims[l] + 1, dims[l + 1], n, F(T.ath[l]), F(T.atl[l]), pn, F(T.dth[cur]),
+                                     F(T.dtl[cur]), pn, SYNK_EPI_STORE, grad + P.woff[l], dims[l + 1], nullptr, nullptr,
+                                     0, nullptr, nullptr, 0, nullptr, nullptr, 0);
+            rc)
+            return rc;
+        if (l == 0) break;
+        const int nxt = cur ^ 1;
+        const bool rows_next = l - 1 >= 1;  // delta_prev feeds another dX product
+        if (int rc = synk_gemm_f32x3(d, n, dims[l], dims[l + 1], F(T.dh[cur]), F(T.dl[cur]), pad4(dims[l + 1]),
+                                     F(T.wh[l]), F(T.wl[l]), pad4(dims[l + 1]), SYNK_EPI_TANH_GRAD, nullptr, 0, nullptr,
+                                     F(T.act[l]), dims[l], rows_next ? F(T.dh[nxt]) : nullptr,
+                                     rows_next ? F(T.dl[nxt]) : nullptr, pad4(dims[l]), F(T.dth[nxt]), F(T.dtl[nxt]),
+                                     pn);
+            rc)
+            return rc;
+        cur = nxt;
+    }
+    return SYNK_OK;
+}
+
+// f32 products on the tensor cores unless SYNK_MLP_F32=ffma (A/B runs).
+bool f32_on_tensor_cores(int compute) {
+    if (compute == SYNK_MLP_F32_TC) return true;
+    const char* e = getenv("SYNK_MLP_F32");  // read per call: tests flip it between runs
+    return !(e && std::string(e) == "ffma");
+}
+
+// Workspace of the native-precision path: the f32 tensor-core plan or the
+// FFMA/DFMA plan.
+uint64_t native_ws(int dtype, int compute, const uint64_t* dims, uint32_t L, const Plan& p, uint64_t n) {
+    if (dtype == SYNK_F32 && f32_on_tensor_cores(compute)) return make_tc_plan(dims, L, n, p.maxd).total;
+    return ws_bytes(dtype, p, n);
 }
 
 // ---- bf16 tensor-core path (config C5: wide MLP, fp32 master weights) -----------------
@@ -688,7 +870,7 @@ namespace {
 // graph; rows != null: index-fused x/y (see loss_grad_t).
 int native_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t layers, const void* params, const void* x,
                      const void* y, uint64_t n, double* loss_dev, void* grad, void* workspace,
-                     uint64_t workspace_bytes, const uint64_t* rows);
+                     uint64_t workspace_bytes, const uint64_t* rows, int compute = SYNK_MLP_NATIVE);
 
 }  // namespace
 
@@ -697,19 +879,25 @@ extern "C" {
 int synk_mlp_workspace_bytes_ex(int dtype, int compute, const uint64_t* dims, uint32_t layers, uint64_t n,
                                 uint64_t* bytes) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "mlp: bad dtype");
-    SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || (compute == SYNK_MLP_BF16_TC && dtype == SYNK_F32), SYNK_EARG,
-                 "mlp: bf16 tensor-core compute needs f32 parameters");
+    SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || (compute == SYNK_MLP_BF16_TC && dtype == SYNK_F32) ||
+                     (compute == SYNK_MLP_F32_TC && dtype == SYNK_F32),
+                 SYNK_EARG, "mlp: tensor-core compute modes need f32 parameters");
     Plan p;
     if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
-    *bytes = compute == SYNK_MLP_NATIVE ? ws_bytes(dtype, p, n) : make_bf16_plan(dims, layers, n, p.maxd).total;
+    *bytes = compute == SYNK_MLP_BF16_TC ? make_bf16_plan(dims, layers, n, p.maxd).total
+                                         : native_ws(dtype, compute, dims, layers, p, n);
     return SYNK_OK;
 }
 
 int synk_mlp_loss_grad_ex(synk_dev* d, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                           const void* params, const void* x, const void* y, uint64_t n, double* loss_dev, void* grad,
                           void* workspace, uint64_t workspace_bytes) {
-    if (compute == SYNK_MLP_NATIVE)
-        return synk_mlp_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes);
+    if (compute == SYNK_MLP_NATIVE || compute == SYNK_MLP_F32_TC) {
+        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || dtype == SYNK_F32, SYNK_EARG,
+                     "mlp: f32 tensor-core compute needs f32 parameters");
+        return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
+                                nullptr, compute);
+    }
     SYNK_REQUIRE(compute == SYNK_MLP_BF16_TC && dtype == SYNK_F32, SYNK_EARG,
                  "mlp: bf16 tensor-core compute needs f32 parameters");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
@@ -728,9 +916,10 @@ int synk_mlp_loss_grad_seg(synk_dev* d, int dtype, int compute, const uint64_t* 
                            const uint64_t* rows) {
     *signalled = 0;
     if (compute != SYNK_MLP_BF16_TC) {
-        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE, SYNK_EARG, "mlp: unknown compute mode");
+        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || (compute == SYNK_MLP_F32_TC && dtype == SYNK_F32), SYNK_EARG,
+                     "mlp: unknown compute mode");
         return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
-                                rows);
+                                rows, compute);
     }
     SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
@@ -762,11 +951,12 @@ int synk_mlp_loss_grad_opts(synk_dev* d, int dtype, int compute, const uint64_t*
     none.signal_base = -1;
     const synk_mlp_opts& o = opts ? *opts : none;
     if (compute != SYNK_MLP_BF16_TC) {
-        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE, SYNK_EARG, "mlp: unknown compute mode");
+        SYNK_REQUIRE(compute == SYNK_MLP_NATIVE || (compute == SYNK_MLP_F32_TC && dtype == SYNK_F32), SYNK_EARG,
+                     "mlp: unknown compute mode");
         if (o.rows && o.rows_ready_on)  // the whole native sequence is one graph: wait up front
             if (int rc = synk_wait_peer_slot(d, o.rows_ready_on, o.rows_ready_slot); rc) return rc;
         return native_loss_grad(d, dtype, dims, layers, params, x, y, n, loss_dev, grad, workspace, workspace_bytes,
-                                o.rows);
+                                o.rows, compute);
     }
     SYNK_REQUIRE(dtype == SYNK_F32, SYNK_EARG, "mlp: bf16 tensor-core compute needs f32 parameters");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
@@ -788,7 +978,7 @@ int synk_mlp_workspace_bytes(int dtype, const uint64_t* dims, uint32_t layers, u
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "mlp: bad dtype");
     Plan p;
     if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
-    *bytes = ws_bytes(dtype, p, n);
+    *bytes = native_ws(dtype, SYNK_MLP_NATIVE, dims, layers, p, n);
     return SYNK_OK;
 }
 
@@ -805,14 +995,19 @@ namespace {
 
 int native_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t layers, const void* params, const void* x,
                      const void* y, uint64_t n, double* loss_dev, void* grad, void* workspace,
-                     uint64_t workspace_bytes, const uint64_t* rows) {
+                     uint64_t workspace_bytes, const uint64_t* rows, int compute) {
     SYNK_REQUIRE(synk::valid_dtype(dtype), SYNK_EDTYPE, "mlp: bad dtype");
     SYNK_REQUIRE(n > 0, SYNK_EARG, "mlp_loss_grad: empty batch");
     Plan p;
     if (int rc = make_plan(dims, layers, n, &p); rc != SYNK_OK) return rc;
-    SYNK_REQUIRE(workspace_bytes >= ws_bytes(dtype, p, n), SYNK_EARG, "mlp: workspace too small");
+    const bool tc = dtype == SYNK_F32 && f32_on_tensor_cores(compute);
+    SYNK_REQUIRE(workspace_bytes >= native_ws(dtype, compute, dims, layers, p, n), SYNK_EARG,
+                 "mlp: workspace too small");
     synk::DeviceGuard g(d->device);
     auto launch_all = [&]() {
+        if (tc)
+            return loss_grad_f32tc(d, dims, layers, p, (const float*)params, (const float*)x, (const float*)y, n,
+                                   loss_dev, (float*)grad, workspace, rows);
         if (dtype == SYNK_F32)
             return loss_grad_t<float>(d, dims, layers, p, (const float*)params, (const float*)x,
                                       (const float*)y, n, loss_dev, (float*)grad, workspace, rows);
@@ -820,7 +1015,7 @@ int native_loss_grad(synk_dev* d, int dtype, const uint64_t* dims, uint32_t laye
                                    (const double*)y, n, loss_dev, (double*)grad, workspace, rows);
     };
     GraphKey key{};
-    key.dtype = dtype;
+    key.dtype = dtype | (tc ? 0x100 : 0);
     key.layers = layers;
     for (uint32_t l = 0; l <= layers && l < 65; ++l) key.dims[l] = dims[l];
     key.n = n;
