@@ -147,20 +147,28 @@ __device__ __forceinline__ void cluster_fold_epilogue(const EpiArgs& epi, float*
     const uint32_t r_end = min((uint32_t)BM, r_begin + rows_per);
     const uint32_t local = (uint32_t)__cvta_generic_to_shared(part);
     float* C = static_cast<float*>(epi.c);
-    constexpr int kQuads = BN / 4;  // float4 columns per row
+    // float4 columns per row that hold output (N = 100: 25 of 32)
+    const uint32_t kQuads = (min((uint32_t)BN, N - n0) + 3) / 4;
     for (uint32_t i = threadIdx.x; i < (r_end - r_begin) * kQuads; i += NT) {
         const uint32_t rr = r_begin + i / kQuads, cc = (i % kQuads) * 4;
         const uint32_t off = local + (rr * kFoldPitch + cc) * 4;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (uint32_t s = 0; s < S; ++s) {
+        // every partial's load in flight before the fold (DSMEM latency is
+        // paid once per item, not S times)
+        float4 x[8];
+#pragma unroll
+        for (uint32_t z = 0; z < 8; ++z) {
+            if (z >= S) break;
             uint32_t remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(off), "r"(s));
-            float x0, x1, x2, x3;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(off), "r"(z));
             asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
-                         : "r"(remote)
-                         : "memory");
-            a0 += (double)x0, a1 += (double)x1, a2 += (double)x2, a3 += (double)x3;
+                         : "=f"(x[z].x), "=f"(x[z].y), "=f"(x[z].z), "=f"(x[z].w)
+                         : "r"(remote));
+        }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (uint32_t z = 0; z < 8; ++z) {
+            if (z >= S) break;
+            a0 += (double)x[z].x, a1 += (double)x[z].y, a2 += (double)x[z].z, a3 += (double)x[z].w;
         }
         const uint64_t m = (uint64_t)m0 + rr;
         if (m >= M) continue;
@@ -181,7 +189,8 @@ template <int KIND, int NT>  // NT = 128 or 256 threads (4 or 8 epilogue warps)
 __global__ void __launch_bounds__(NT, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a0, const __grid_constant__ CUtensorMap a1,
                    const __grid_constant__ CUtensorMap b0, const __grid_constant__ CUtensorMap b1, int passes,
-                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per, uint32_t layout, int cfold) {
+                   uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t kb_per, uint32_t layout, int cfold,
+                   uint32_t n_eff) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(NT, 2)
             const CUtensorMap* ma = pass == 2 ? &a1 : &a0;  // passes: hi.hi, hi.lo, lo.hi
             const CUtensorMap* mb = pass == 1 ? &b1 : &b0;
             const uint32_t full = smem_u32(&bars[s]);
-            mbar_expect_tx(full, 2 * kTileBytes);
+            mbar_expect_tx(full, kTileBytes + n_eff * 128);  // B box: n_eff rows (narrow N) x 128 B
             const int kc = (kb0 + kb) * kBK;
             if (layout & kAMn) {  // two 64(M) x 64(K) boxes
                 tma_load_2d(smem_u32(sa + s * kTileBytes), ma, full, (int)m0, kc);
@@ -252,7 +261,9 @@ __global__ void __launch_bounds__(NT, 2)
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
         const bool amn = layout & kAMn, bmn = layout & kBMn;
-        const uint32_t idesc = instr_desc<KIND>() | (amn ? 1u << 15 : 0u) | (bmn ? 1u << 16 : 0u);
+        // UMMA N = n_eff (BN, or N rounded up to 16 for a narrow K-major B)
+        const uint32_t idesc = (instr_desc<KIND>() & ~(0x3Fu << 17)) | ((n_eff >> 3) << 17) | (amn ? 1u << 15 : 0u) |
+                               (bmn ? 1u << 16 : 0u);
         for (int it = 0; it < total; ++it) {
             const int s = it % kStages;
             mbar_wait(smem_u32(&bars[s]), (it / kStages) & 1);
@@ -741,7 +752,7 @@ constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
-           uint32_t kb_per = 0x7fffffffu, uint32_t layout = 0, int cfold = 0) {
+           uint32_t kb_per = 0x7fffffffu, uint32_t layout = 0, int cfold = 0, uint32_t n_eff = BN) {
     // Epilogue-heavy launches (short K, or the tanh-derivative reading the
     // activation tile) get 8 epilogue warps; MMA-bound ones keep 4 warps and
     // the full register budget. SYNK_GEMM_WARPS=4|8 overrides (A/B runs).
@@ -767,19 +778,19 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         SYNK_CU(cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N, (uint32_t)K, e, kb_per,
-                                   layout, 1));
+                                   layout, 1, n_eff));
         return SYNK_OK;
     }
     if (wide) {
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 256>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 256><<<grid, 256, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per, layout, 0);
+                                                                       (uint32_t)K, e, kb_per, layout, 0, n_eff);
     } else {
         if (int rc = synk::ensure_max_smem((const void*)gemm_tc_kernel<KIND, 128>, d->device, (int)kSmemBytes); rc)
             return rc;
         gemm_tc_kernel<KIND, 128><<<grid, 128, kSmemBytes, d->stream>>>(a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N,
-                                                                       (uint32_t)K, e, kb_per, layout, 0);
+                                                                       (uint32_t)K, e, kb_per, layout, 0, n_eff);
     }
     SYNK_LAUNCHED("gemm_tc_kernel");
     return SYNK_OK;
@@ -1035,6 +1046,18 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
         return SYNK_OK;
     }
+    // Narrow N (one column tile) with a K-major B: UMMA N = N rounded up to 16
+    // and a B box of that many rows, so the zero rows the 128-row tile would
+    // add are neither moved into shared memory nor multiplied (C5's N = 100
+    // products: 112 instead of 128 B rows per stage).
+    uint32_t n_eff = BN;
+    if (N < BN && !(lay & kBMn)) {
+        n_eff = (uint32_t)((N + 15) / 16 * 16);
+        if (int rc = make_map(&b0, b_hi, N, K, ldb, bf16, n_eff); rc) return rc;
+        b1 = b0;
+        if (kind == 2)
+            if (int rc = make_map(&b1, b_lo, N, K, ldb, false, n_eff); rc) return rc;
+    }
     // Too few output tiles to fill the GPU and a long K: split K over grid.z
     // (fixed split for a given shape, so results do not depend on the device),
     // fp32 partial planes in a stream-ordered scratch, one fold kernel.
@@ -1071,7 +1094,7 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         if (cluster_fold && bf16 && splits <= 8) {
             EpiArgs ce{epilogue == SYNK_EPI_BIAS ? EPI_BIAS : EPI_STORE, 0, c, ldc, nullptr, 0,
                        epilogue == SYNK_EPI_BIAS ? bias : nullptr, nullptr, 0};
-            const int rc = launch<0>(d, 1, a0, a1, b0, b1, M, N, K, ce, splits, kb_per, lay, 1);
+            const int rc = launch<0>(d, 1, a0, a1, b0, b1, M, N, K, ce, splits, kb_per, lay, 1, n_eff);
             if (rc == SYNK_OK) return rc;
             // a cluster of `splits` CTAs that cannot be scheduled here (e.g. an
             // SM-limited context): clear the launch error, take the planes path
@@ -1080,8 +1103,8 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         float* planes = nullptr;
         SYNK_CU(cudaMallocAsync((void**)&planes, (size_t)splits * M * N * sizeof(float), d->stream));
         EpiArgs pe{SYNK_EPI_STORE, 0, planes, N, nullptr, 0, nullptr, nullptr, 0};
-        int rc = bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per, lay)
-                      : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per);
+        int rc = bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per, lay, 0, n_eff)
+                      : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, pe, splits, kb_per, 0, 0, n_eff);
         if (rc) return rc;
         const unsigned fgrid = (unsigned)std::min<uint64_t>((M * N + 255) / 256, (uint64_t)d->num_sms * 8);
         splitk_fold_kernel<<<fgrid, 256, 0, d->stream>>>(splits, M, N, planes, static_cast<float*>(c), ldc,
@@ -1090,8 +1113,8 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         SYNK_CU(cudaFreeAsync(planes, d->stream));
         return SYNK_OK;
     }
-    return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e, 1, 0x7fffffffu, lay)
-                : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, e);
+    return bf16 ? launch<0>(d, 1, a0, a1, b0, b1, M, N, K, e, 1, 0x7fffffffu, lay, 0, n_eff)
+                : launch<1>(d, kind == 2 ? 3 : 1, a0, a1, b0, b1, M, N, K, e, 1, 0x7fffffffu, 0, 0, n_eff);
 }
 
 }  // extern "C"
