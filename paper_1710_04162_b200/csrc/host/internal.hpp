@@ -13,12 +13,24 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "synk_cuda.h"
 #include "synkpar/device.hpp"
 #include "synkpar/function.hpp"
 #include "synkpar/worker_pool.hpp"
 
 namespace synkpar::detail {
+
+// NVTX range for profiler timelines (nsys / ncu --nvtx): header-only NVTX3,
+// a no-op unless a tool injects itself. Names: "synk.<phase>" per rank task,
+// "synk.<api>" for the public entry points.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct FunctionCore;
 struct PoolState;

@@ -178,6 +178,7 @@ std::size_t ReplicatedVariable::world() const { return live(rec_, "world").repli
 DType ReplicatedVariable::dtype() const { return live(rec_, "dtype").replicas.at(0).dtype(); }
 
 void ReplicatedVariable::broadcast(std::size_t src) {
+    detail::NvtxRange range("synk.broadcast");
     detail::VarRecord& rec = live_full(rec_, "broadcast");
     rec.mutated();
     check_rank(rec, src, "broadcast");
@@ -222,6 +223,7 @@ void ReplicatedVariable::broadcast(std::size_t src) {
 }
 
 void ReplicatedVariable::all_reduce(ReduceOp op) {
+    detail::NvtxRange range("synk.all_reduce");
     detail::VarRecord& rec = live_full(rec_, "all_reduce");
     rec.mutated();
     not_gather(op, "all_reduce");

@@ -457,6 +457,7 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
 
 double SyncSgd::train_step(const ParallelFunction& f_grad, const std::vector<FunctionArg>& batch,
                            const CallOptions& call_opts) {
+    detail::NvtxRange range("synk.train_step");
     const auto t0 = Clock::now();
     StepReport rep;
     auto st = detail::state_of(*pool_);
