@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
                      "r"(2 * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    __syncwarp();  // warp 0 reconverges after thread 0's barrier init: bar.sync is .aligned
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -415,13 +416,22 @@ __global__ void __launch_bounds__(256) tf32_stage_kernel(SplitBatch batch, synk_
     split_tile(job, (uint64_t)(t / tiles_x) * 32, (uint64_t)(t % tiles_x) * 32, tile);
 }
 
-uint32_t choose_splits(uint64_t M, uint64_t N, uint64_t K, int bn, uint32_t* kb_per) {
+// Split-K depth S (the cluster size along z). Fixed by the shape and the
+// CTA footprint, never by the device, so results are device-independent. The
+// clusters must also fit in ONE wave: cluster CTAs are placed inside a GPC
+// (148 SMs = 8 GPCs), and 16 clusters of 7 did not fit at one CTA per SM, so
+// the bound used is 8 * floor(12 / S) clusters of S
+// single-CTA SMs (twice that at two CTAs per SM); a cluster
+// left for a second wave doubles the launch (measured: CTA start times spread
+// over 11.9 us with 16 clusters of 7 at one CTA per SM).
+uint32_t choose_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int ctas_per_sm, uint32_t* kb_per) {
     const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
     const uint64_t num_kb = (K + BK - 1) / BK;
-    uint64_t s = 148 / tiles;  // one CTA per SM: fill a 148-SM B200 (fixed: device-independent results)
+    uint64_t s = 148 / tiles;  // fill a 148-SM B200
     s = std::min<uint64_t>(s, 8);
     s = std::min<uint64_t>(s, num_kb);
     s = std::max<uint64_t>(s, 1);
+    while (s > 1 && tiles > 8 * (12 / s) * (uint64_t)ctas_per_sm) --s;
     const uint64_t per = (num_kb + s - 1) / s;
     *kb_per = (uint32_t)per;
     return (uint32_t)((num_kb + per - 1) / per);
@@ -441,8 +451,8 @@ int launch_f32x3(synk_dev* d, const CUtensorMap& ah, const CUtensorMap& al, cons
     if (act_tma)
         if (int rc = make_map(&ta, o.act, M, N, o.ldact, false, 128); rc) return rc;
     uint32_t kb_per = 0;
-    const uint32_t S = choose_splits(M, N, K, BN, &kb_per);
     const size_t smem = C::smem(act_tma);
+    const uint32_t S = choose_splits(M, N, K, BN, smem <= 113 * 1024 ? 2 : 1, &kb_per);
     if (int rc = synk::ensure_max_smem((const void*)gemm_f32x3_kernel<BN, EK>, d->device, (int)C::smem(true)); rc)
         return rc;
     cudaLaunchConfig_t cfg = {};

@@ -841,6 +841,9 @@ int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
     const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ei != cudaSuccess) return synk::cuda_fail(ei, "cudaGraphInstantiate (mlp loss/grad)");
+    // Upload the executable graph now: replays then only submit it (the first
+    // launch would otherwise carry the upload).
+    SYNK_CU(cudaGraphUpload(exec, d->stream));
     if (gc.entries.size() == GraphCache::kMax) {
         auto lru = std::min_element(gc.entries.begin(), gc.entries.end(),
                                     [](const GraphCache::Entry& a, const GraphCache::Entry& b) { return a.used < b.used; });
