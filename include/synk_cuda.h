@@ -422,7 +422,13 @@ int synk_mlp_loss_grad_seg(synk_dev* dev, int dtype, int compute, const uint64_t
  *                    another buffer (double-buffered shadows), so segment l is
  *                    signalled right after its weight gradient; 0: the update
  *                    rewrites this shadow, so segment l (l > 0) is signalled
- *                    only after dX_l has read W_l. */
+ *                    only after dX_l has read W_l.
+ *   seg_order        out (may be NULL, else >= layers ints): the layer of
+ *                    each signalled segment, in signal order. The bf16 path
+ *                    runs every dX product first and then the weight
+ *                    gradients largest segment first, so each segment's
+ *                    all-reduce + update overlaps the remaining weight-
+ *                    gradient products. */
 typedef struct synk_mlp_opts {
     int signal_base;
     const uint64_t* rows;
@@ -432,6 +438,7 @@ typedef struct synk_mlp_opts {
     void* shadow;
     int shadow_valid;
     int shadow_spare;
+    int* seg_order;
 } synk_mlp_opts;
 int synk_mlp_loss_grad_opts(synk_dev* dev, int dtype, int compute, const uint64_t* dims, uint32_t layers,
                             const void* params, const void* x, const void* y, uint64_t n, double* loss_dev,

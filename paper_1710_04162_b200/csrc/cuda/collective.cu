@@ -29,6 +29,12 @@ using synk::combine_op;
 
 constexpr int kMaxWorld = 64;
 constexpr int kBlock = 256;
+// The fused all-reduce + update runs beside the persistent GEMM (overlapped
+// segment updates): 384 GEMM threads x 128 registers leave 16K registers per
+// SM, so 128-thread CTAs (74 registers) can co-reside and start as soon as
+// their segment is final; 256-thread CTAs could not, and waited for GEMM CTAs
+// to retire (C5: the W_1 update started 60 us into the next GEMM).
+constexpr int kStepBlock = 128;
 
 struct Ptrs {
     void* p[kMaxWorld];
@@ -255,77 +261,96 @@ __device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t g
     }
 }
 
-template <class T, int W, int BYTES, bool SH>
-__device__ __forceinline__ void step_vector(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
-                                            int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
-                                            int naux, uint64_t v, const Shadow& sh, bool grads_local) {
+// U vector items per call (v[u], valid while v[u] < v_end): every load of
+// every item (W gradient replicas, params, aux) is issued before the first
+// use, so a thread has U x (W + 1 + naux) 16/32-byte loads in flight instead
+// of one dependent round trip per array -- the update runs beside the
+// persistent GEMMs with one 128-thread CTA per SM, where memory-level
+// parallelism per thread sets its bandwidth.
+template <class T, int W, int BYTES, bool SH, int U>
+__device__ __forceinline__ void step_vectors(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
+                                             int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
+                                             int naux, uint64_t v0, uint64_t vstride, uint64_t v_end, const Shadow& sh,
+                                             bool grads_local) {
     using V = VecT<T, BYTES>;
     constexpr int N = V::N;
-    V gx[W];
+    V gx[U][W], p[U], a0[U], a1[U];
 #pragma unroll
-    for (int q = 0; q < W; ++q) gx[q] = vload<T, BYTES>(grads.p[q], v);
-    V g;
+    for (int u = 0; u < U; ++u) {
+        const uint64_t v = v0 + u * vstride;
+        if (v >= v_end) continue;
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        T e[W];
-#pragma unroll
-        for (int q = 0; q < W; ++q) e[q] = gx[q].e[k];
-        g.e[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
+        for (int q = 0; q < W; ++q) gx[u][q] = vload<T, BYTES>(grads.p[q], v);
+        p[u] = vload<T, BYTES>(params.p[rank], v);
+        if (naux > 0) a0[u] = vload<T, BYTES>(aux0.p[rank], v);
+        if (naux > 1) a1[u] = vload<T, BYTES>(aux1.p[rank], v);
     }
-    if constexpr (W > 1) {
-        if (grads_local) {  // deferred all-gather: the chunk stays with its owner
-            vstore<T, BYTES>(grads.p[rank], v, g);
-        } else {
 #pragma unroll
-            for (int q = 0; q < W; ++q) vstore<T, BYTES>(grads.p[q], v, g);
+    for (int u = 0; u < U; ++u) {
+        const uint64_t v = v0 + u * vstride;
+        if (v >= v_end) continue;
+        V g;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            T e[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) e[q] = gx[u][q].e[k];
+            g.e[k] = finish_mean(grad_op, tree_fold_regs<T, W>(fop, e), inv_w);
         }
-    }
-    V p = vload<T, BYTES>(params.p[rank], v);
-    V a0 = naux > 0 ? vload<T, BYTES>(aux0.p[rank], v) : p;
-    V a1 = naux > 1 ? vload<T, BYTES>(aux1.p[rank], v) : p;
+        if constexpr (W > 1) {
+            if (grads_local) {  // deferred all-gather: the chunk stays with its owner
+                vstore<T, BYTES>(grads.p[rank], v, g);
+            } else {
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        double pd = (double)p.e[k];
-        double x0 = (double)a0.e[k];
-        double x1 = (double)a1.e[k];
-        synk::rule_update(rp, pd, x0, x1, (double)g.e[k]);
-        p.e[k] = (T)pd;
-        a0.e[k] = (T)x0;
-        a1.e[k] = (T)x1;
-    }
+                for (int q = 0; q < W; ++q) vstore<T, BYTES>(grads.p[q], v, g);
+            }
+        }
+        V pn = p[u], x0 = naux > 0 ? a0[u] : p[u], x1 = naux > 1 ? a1[u] : p[u];
 #pragma unroll
-    for (int q = 0; q < W; ++q) {
-        vstore<T, BYTES>(params.p[q], v, p);
-        if (naux > 0) vstore<T, BYTES>(aux0.p[q], v, a0);
-        if (naux > 1) vstore<T, BYTES>(aux1.p[q], v, a1);
-        if constexpr (SH) shadow_store<N>(sh, q, sh.elem_base + v * N, reinterpret_cast<const float*>(p.e));
+        for (int k = 0; k < N; ++k) {
+            double pd = (double)pn.e[k];
+            double d0 = (double)x0.e[k];
+            double d1 = (double)x1.e[k];
+            synk::rule_update(rp, pd, d0, d1, (double)g.e[k]);
+            pn.e[k] = (T)pd;
+            x0.e[k] = (T)d0;
+            x1.e[k] = (T)d1;
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+            vstore<T, BYTES>(params.p[q], v, pn);
+            if (naux > 0) vstore<T, BYTES>(aux0.p[q], v, x0);
+            if (naux > 1) vstore<T, BYTES>(aux1.p[q], v, x1);
+            if constexpr (SH) shadow_store<N>(sh, q, sh.elem_base + v * N, reinterpret_cast<const float*>(pn.e));
+        }
     }
 }
 
 template <class T, int W, bool SH>
-__global__ void __launch_bounds__(kBlock) allreduce_step_kernel(
+__global__ void __launch_bounds__(kStepBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
     double inv_w, synk::RuleParams rp, int naux, bool coherent, bool grads_local, uint64_t lo, uint64_t hi,
     int vec_bytes, Shadow sh) {
     const int fop = grad_op == SYNK_OP_MEAN ? SYNK_OP_SUM : grad_op;
-    uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
-    uint64_t stride = (uint64_t)gridDim.x * kBlock;
+    uint64_t tid = (uint64_t)blockIdx.x * kStepBlock + threadIdx.x;
+    uint64_t stride = (uint64_t)gridDim.x * kStepBlock;
     if constexpr (W > 0) {
         if (vec_bytes && coherent) {
             // lo is 16-element aligned, so a multiple of both vector widths
+            constexpr int U = W <= 2 ? 2 : 1;  // items in flight per thread (registers: W + 3 vectors each)
             if (vec_bytes == 32) {
                 constexpr int N = VecT<T, 32>::N;
                 const uint64_t v0 = lo / N, v1 = hi / N;
-                for (uint64_t v = v0 + tid; v < v1; v += stride)
-                    step_vector<T, W, 32, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh,
-                                              grads_local);
+                for (uint64_t v = v0 + tid; v < v1; v += stride * U)
+                    step_vectors<T, W, 32, SH, U>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v,
+                                                  stride, v1, sh, grads_local);
                 lo = v1 * N;  // scalar tail below
             } else {
                 constexpr int N = VecT<T, 16>::N;
                 const uint64_t v0 = lo / N, v1 = hi / N;
-                for (uint64_t v = v0 + tid; v < v1; v += stride)
-                    step_vector<T, W, 16, SH>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, sh,
-                                              grads_local);
+                for (uint64_t v = v0 + tid; v < v1; v += stride * U)
+                    step_vectors<T, W, 16, SH, U>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v,
+                                                  stride, v1, sh, grads_local);
                 lo = v1 * N;
             }
         }
@@ -490,7 +515,9 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     }();
     const int vec_bytes = aligned(32) && forced != 16 ? 32 : (aligned(16) ? 16 : 0);
     const uint64_t items = vec_bytes ? (hi - lo) / (vec_bytes / sizeof(T)) + 1 : hi - lo;
-    unsigned grid = synk::grid_for(d, items, kBlock);
+    // at most 4 CTAs per SM (37K registers): beside them the next narrow GEMM
+    // still fits its two CTAs per SM (94 registers x 128 threads each)
+    unsigned grid = synk::grid_for(d, items, kStepBlock, 8);
     if (flags & SYNK_STEP_BACKGROUND) {
         // Overlapped with tensor-core GEMMs on the other stream: a few CTAs
         // stream the segment at a fraction of HBM bandwidth instead of
@@ -508,19 +535,24 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     switch (w) {
 #define SYNK_ARS_CASE(WW)                                                                                        \
     case WW:                                                                                                     \
-        if (with)                                                                                                \
-            allreduce_step_kernel<T, WW, true><<<grid, kBlock, 0, d->stream>>>(                                  \
+        if (with) {                                                                                              \
+            if (int rc = synk::prefer_shared_carveout((const void*)allreduce_step_kernel<T, WW, true>, d->device); rc) \
+                return rc;                                                                                       \
+            allreduce_step_kernel<T, WW, true><<<grid, kStepBlock, 0, d->stream>>>(                                  \
                 P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
-        else                                                                                                     \
-            allreduce_step_kernel<T, WW, false><<<grid, kBlock, 0, d->stream>>>(                                 \
+        } else {                                                                                                 \
+            if (int rc = synk::prefer_shared_carveout((const void*)allreduce_step_kernel<T, WW, false>, d->device); rc) \
+                return rc;                                                                                       \
+            allreduce_step_kernel<T, WW, false><<<grid, kStepBlock, 0, d->stream>>>(                                 \
                 P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
+        }                                                                                                        \
         break;
         SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(3) SYNK_ARS_CASE(4)
         SYNK_ARS_CASE(5) SYNK_ARS_CASE(6) SYNK_ARS_CASE(7) SYNK_ARS_CASE(8)
 #undef SYNK_ARS_CASE
     default:
         SYNK_REQUIRE(!with, SYNK_EARG, "all_reduce_step: bf16 shadows need world <= 8");
-        allreduce_step_kernel<T, 0, false><<<grid, kBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
+        allreduce_step_kernel<T, 0, false><<<grid, kStepBlock, 0, d->stream>>>(P, G, A0, A1, w, d->rank, grad_op,
                                                                            inv_w, rp, naux, coherent, grads_local, lo, hi, 0,
                                                                            S);
     }

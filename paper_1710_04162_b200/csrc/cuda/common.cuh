@@ -39,6 +39,9 @@ int cuda_fail(cudaError_t err, const char* what);
 // attribute is per-device state (each GPU's context has its own copy of the
 // function), so it is set once per (kernel, device) pair, thread-safely.
 int ensure_max_smem(const void* kernel, int device, int bytes);
+// Largest shared-memory carveout for a kernel that runs beside max-smem GEMMs
+// (no SM reconfiguration drain between them); once per (kernel, device).
+int prefer_shared_carveout(const void* kernel, int device);
 
 // Releases the rank's graph cache (mlp.cu); called by synk_close.
 void release_graphs(synk_dev* d);

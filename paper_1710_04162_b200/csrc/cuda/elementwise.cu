@@ -469,6 +469,7 @@ int synk_copy_small(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
     if (bytes == 0) return SYNK_OK;
     SYNK_REQUIRE(bytes <= (1u << 20), SYNK_EARG, "synk_copy_small: at most 1 MiB");
     synk::DeviceGuard g(d->device);
+    if (int rc = synk::prefer_shared_carveout((const void*)copy_small_kernel, d->device); rc) return rc;
     copy_small_kernel<<<1, 256, 0, d->stream>>>((char*)dst, (const char*)src, bytes);
     SYNK_LAUNCHED("copy_small_kernel");
     return SYNK_OK;

@@ -536,97 +536,177 @@ __device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64
 // already accumulates tile i+1.
 // 12 warps: 0 TMA, 1 MMA, 2 TMEM allocator, 3 idle, 4..11 epilogue (two warps
 // per TMEM lane quadrant, each draining half of the 256 accumulator columns).
-constexpr int PBN = 256, PStages = 4, PThreads = 384, PEpiThreads = 256;
-constexpr int PA = 128 * 128, PB = 256 * 128;  // bytes per stage: A 128 rows, B 256 rows, 128 B each
+//
+// PAIR = 2: a CTA pair (cluster of 2 on one TPC) computes 256 x 256 tiles with
+// tcgen05.mma.cta_group::2 issued by the even CTA: each CTA stages its own 128
+// rows of A and 128 of the 256 B rows (32 KB per stage instead of 48: six
+// stages, a third less L2 -> SM traffic per flop), the TMA loads of both CTAs
+// complete on the leader's full barrier, the MMA commits arrive on both CTAs'
+// barriers (multicast), and each CTA drains its own 128 accumulator rows from
+// its own TMEM; the leader's TMEM-empty barrier counts both CTAs' epilogue warps.
+constexpr int PBN = 256, PThreads = 384, PEpiThreads = 256;
+template <int PAIR>
+struct PCfg {
+    static constexpr int kStages = PAIR == 2 ? 6 : 4;
+    static constexpr int kA = 128 * 128;                // bytes per stage: this CTA's 128 A rows
+    static constexpr int kB = (PBN / PAIR) * 128;       // this CTA's B rows (256 or 128), 128 B each
+    static constexpr int kTileM = 128 * PAIR;
+    static constexpr size_t kSmem = (size_t)kStages * (kA + kB) + 1024 + 256;
+};
+constexpr int PStages = PCfg<1>::kStages;  // (1-CTA layout, host-side sizes)
+constexpr int PA = PCfg<1>::kA, PB = PCfg<1>::kB;
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// TMA load whose completion is counted on the pair leader's barrier (bar is a
+// shared::cluster address in the leader CTA).
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// commit the leader's MMAs to the barrier at `bar`'s offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+            bar)
+        : "memory");
+}
+
+template <int PAIR>
 __global__ void __launch_bounds__(PThreads, 1)
     gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                               uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t layout) {
+    using PC = PCfg<PAIR>;
+    constexpr int kStages = PC::kStages, kA = PC::kA, kB = PC::kB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sa = smem;
-    uint8_t* sb = smem + PStages * PA;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + PStages * PB);
-    uint64_t* full = bars;                 // [PStages]
-    uint64_t* empty = bars + PStages;      // [PStages]
-    uint64_t* tfull = bars + 2 * PStages;  // [2]
+    uint8_t* sb = smem + kStages * kA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * kB);
+    uint64_t* full = bars;                 // [kStages]
+    uint64_t* empty = bars + kStages;      // [kStages]
+    uint64_t* tfull = bars + 2 * kStages;  // [2]
     uint64_t* tempty = tfull + 2;          // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t rank = PAIR == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const uint32_t unit = blockIdx.x / PAIR, units = gridDim.x / PAIR;  // pair (or CTA) index / count
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     constexpr int kBK = 64;  // bf16 elements per 128-byte K block
-    const uint32_t num_m = (M + BM - 1) / BM, num_n = (N + PBN - 1) / PBN;
+    const uint32_t num_m = (M + PC::kTileM - 1) / PC::kTileM, num_n = (N + PBN - 1) / PBN;
     const uint32_t tiles = num_m * num_n;
     const int num_kb = (int)((K + kBK - 1) / kBK);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < PStages; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
             mbar_init(smem_u32(&empty[s]), 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&tfull[b]), 1);
-            mbar_init(smem_u32(&tempty[b]), PEpiThreads);  // every epilogue thread arrives
+            // every epilogue warp of the pair arrives (one elected lane each)
+            mbar_init(smem_u32(&tempty[b]), PAIR * (PEpiThreads / 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&ta);
         prefetch_map(&tb);
     }
+    __syncwarp();
+    // the pair's TMEM allocation touches both SMs' allocator state: both CTAs
+    // must be running (and past their prologue) before either allocates
+    if constexpr (PAIR == 2) cluster_sync_all();
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(2 * PBN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(2 * PBN));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(2 * PBN));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR == 2) cluster_sync_all();  // the peer's barriers exist before any remote arrive / TMA signal
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
-        // ---- TMA producer ----
+        // ---- TMA producer (both CTAs: this CTA's A rows and B rows) ----
         uint32_t it = 0;
-        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-            const int m0 = (int)((t / num_n) * BM), n0 = (int)((t % num_n) * PBN);
+        for (uint32_t t = unit; t < tiles; t += units) {
+            const int m0 = (int)((t / num_n) * PC::kTileM + rank * 128), n0 = (int)((t % num_n) * PBN + rank * (PBN / PAIR));
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
-                const int s = it % PStages;
-                mbar_wait(smem_u32(&empty[s]), ((it / PStages) & 1) ^ 1);
-                mbar_expect_tx(smem_u32(&full[s]), PA + PB);
+                const int s = it % kStages;
+                mbar_wait(smem_u32(&empty[s]), ((it / kStages) & 1) ^ 1);
+                uint32_t fb = smem_u32(&full[s]);
+                if (leader) mbar_expect_tx(fb, PAIR * (kA + kB));  // both CTAs' bytes land on the leader's barrier
+                if constexpr (PAIR == 2) fb = map_to_rank(fb, 0);
+                auto load = [&](uint32_t dst, const CUtensorMap* map, int x, int y) {
+                    if constexpr (PAIR == 2) tma_load_2d_pair(dst, map, fb, x, y);
+                    else tma_load_2d(dst, map, fb, x, y);
+                };
                 if (layout & kAMn) {  // 64(M) x 64(K) boxes along M
-                    for (int j = 0; j < BM / 64; ++j)
-                        tma_load_2d(smem_u32(sa + s * PA + j * 8192), &ta, smem_u32(&full[s]), m0 + 64 * j, kb * kBK);
+                    for (int j = 0; j < 128 / 64; ++j) load(smem_u32(sa + s * kA + j * 8192), &ta, m0 + 64 * j, kb * kBK);
                 } else {
-                    tma_load_2d(smem_u32(sa + s * PA), &ta, smem_u32(&full[s]), kb * kBK, m0);
+                    load(smem_u32(sa + s * kA), &ta, kb * kBK, m0);
                 }
                 if (layout & kBMn) {
-                    for (int j = 0; j < PBN / 64; ++j)
-                        tma_load_2d(smem_u32(sb + s * PB + j * 8192), &tb, smem_u32(&full[s]), n0 + 64 * j, kb * kBK);
+                    for (int j = 0; j < PBN / PAIR / 64; ++j)
+                        load(smem_u32(sb + s * kB + j * 8192), &tb, n0 + 64 * j, kb * kBK);
                 } else {
-                    tma_load_2d(smem_u32(sb + s * PB), &tb, smem_u32(&full[s]), kb * kBK, n0);
+                    load(smem_u32(sb + s * kB), &tb, kb * kBK, n0);
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer ----
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ---- MMA issuer (the pair leader: UMMA M = 128 * PAIR) ----
         const bool amn = layout & kAMn, bmn = layout & kBMn;
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (amn ? 1u << 15 : 0u) | (bmn ? 1u << 16 : 0u) |
-                               ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                               ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(PC::kTileM >> 4) << 24);
         uint32_t it = 0, tl = 0;
-        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        for (uint32_t t = unit; t < tiles; t += units, ++tl) {
             const uint32_t acc = tl & 1;
-            mbar_wait(smem_u32(&tempty[acc]), ((tl >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            mbar_wait(smem_u32(&tempty[acc]), ((tl >> 1) & 1) ^ 1);  // both CTAs drained this buffer
             tc_fence_after();
             const uint32_t d = tmem + acc * PBN;
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
-                const int s = it % PStages;
-                mbar_wait(smem_u32(&full[s]), (it / PStages) & 1);
+                const int s = it % kStages;
+                mbar_wait(smem_u32(&full[s]), (it / kStages) & 1);
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(sa + s * PA), b_base = smem_u32(sb + s * PB);
+                const uint32_t a_base = smem_u32(sa + s * kA), b_base = smem_u32(sb + s * kB);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    umma<0>(d, op_desc(a_base, k, amn), op_desc(b_base, k, bmn), idesc, (kb > 0 || k > 0) ? 1u : 0u);
-                umma_commit(smem_u32(&empty[s]));
+                for (int k = 0; k < 4; ++k) {
+                    if constexpr (PAIR == 2)
+                        umma_pair(d, op_desc(a_base, k, amn), op_desc(b_base, k, bmn), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    else
+                        umma<0>(d, op_desc(a_base, k, amn), op_desc(b_base, k, bmn), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                }
+                if constexpr (PAIR == 2) umma_commit_pair(smem_u32(&empty[s]));
+                else umma_commit(smem_u32(&empty[s]));
             }
-            umma_commit(smem_u32(&tfull[acc]));
+            if constexpr (PAIR == 2) umma_commit_pair(smem_u32(&tfull[acc]));
+            else umma_commit(smem_u32(&tfull[acc]));
         }
     } else if (warp >= 4) {
         // ---- epilogue: warps 4..11; warp w owns TMEM lane quadrant w % 4 and
@@ -640,10 +720,20 @@ __global__ void __launch_bounds__(PThreads, 1)
         // 32-byte alignment of every 16-column chunk (bf16: 32 B) for the 256-bit paths
         const bool act32 = pre_ok && (epi.ldact * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(epi.act) & 31) == 0;
         const bool c32 = pre_ok && epi.c && (epi.ldc * 2) % 32 == 0 && (reinterpret_cast<uintptr_t>(epi.c) & 31) == 0;
+        // TMEM-empty arrival: one elected lane per warp, on the pair leader's barrier
+        const uint32_t tempty_at[2] = {PAIR == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]),
+                                       PAIR == 2 ? map_to_rank(smem_u32(&tempty[1]), 0) : smem_u32(&tempty[1])};
+        auto drained = [&](uint32_t acc) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_at[acc])
+                             : "memory");
+        };
         uint32_t tl = 0;
-        for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        for (uint32_t t = unit; t < tiles; t += units, ++tl) {
             const uint32_t acc = tl & 1;
-            const uint64_t m0 = (t / num_n) * BM, n0 = (uint64_t)(t % num_n) * PBN;
+            const uint64_t m0 = (t / num_n) * PC::kTileM + rank * 128, n0 = (uint64_t)(t % num_n) * PBN;
             const uint64_t m = m0 + quad * 32 + lane;
             const uint32_t base = tmem + acc * PBN + ((uint32_t)(quad * 32) << 16);
             const int cbeg = half * (PBN / 2), cend = cbeg + PBN / 2;
@@ -700,8 +790,7 @@ __global__ void __launch_bounds__(PThreads, 1)
                                                             a[2 * k], a[2 * k + 1]);
                     }
                 }
-                tc_fence_before();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+                drained(acc);
                 continue;
             }
             mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
@@ -717,14 +806,18 @@ __global__ void __launch_bounds__(PThreads, 1)
                 tmem_ld16(base + c0, r);
                 if (m < M && n0 + c0 < N) epi_chunk(epi, m, n0 + c0, N, r, vec_c, vec_act, have, cur0, cur1);
             }
-            tc_fence_before();
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[acc])) : "memory");
+            drained(acc);
         }
     }
     __syncwarp();
     tc_fence_before();
-    __syncthreads();
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * PBN));
+    if constexpr (PAIR == 2) {
+        cluster_sync_all();  // both CTAs done with the pair's TMEM before it is freed
+        if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * PBN));
+    } else {
+        __syncthreads();
+        if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * PBN));
+    }
 }
 
 // ---- host side: tensor maps ---------------------------------------------------------
@@ -963,6 +1056,7 @@ int synk_gemm_prep2_bf16_rows(synk_dev* d, const float* in, const uint64_t* rowm
         // cast only: the vectorised streaming kernel (no shared-memory tile)
         const uint64_t total = rows * (cols / 8);
         const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, (uint64_t)d->num_sms * 8);
+        if (int rc = synk::prefer_shared_carveout((const void*)cast_bf16_rows_kernel, d->device); rc) return rc;
         cast_bf16_rows_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out),
                                                            ld_out);
         SYNK_LAUNCHED("cast_bf16_rows_kernel");
@@ -970,6 +1064,7 @@ int synk_gemm_prep2_bf16_rows(synk_dev* d, const float* in, const uint64_t* rowm
     }
     dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
     const int vec_in = (ld_in % 4 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
+    if (int rc = synk::prefer_shared_carveout((const void*)prep2_bf16_kernel, d->device); rc) return rc;
     prep2_bf16_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out), ld_out,
                                                    static_cast<__nv_bfloat16*>(out_t), ld_out_t, vec_in, rowmap);
     SYNK_LAUNCHED("prep2_bf16_kernel");
@@ -1034,15 +1129,46 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         return v ? atoi(v) : 1;
     }();
     if (bf16 && persistent_mode && N > 128) {
+        // CTA-pair (cta_group::2) 256 x 256 tiles: +6-9 % over the 1-CTA
+        // 128 x 256 kernel on C5's shapes with random operands (1,479 vs 1,391
+        // TFLOP/s at 8192x4096x4096), C5 step 1.127 -> 1.071 ms
+        // (profiles/r02_gemm_pair.txt). SYNK_GEMM_PAIR=0: the 1-CTA kernel.
+        static const bool pair = [] {
+            const char* v = getenv("SYNK_GEMM_PAIR");
+            return !(v && v[0] == '0');
+        }();
         CUtensorMap bw = b0;
         if (!(lay & kBMn))
-            if (int rc = make_map(&bw, b_hi, N, K, ldb, true, PBN); rc) return rc;
-        constexpr size_t smem = (size_t)PStages * (PA + PB) + 1024 + 256;
-        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel, d->device, (int)smem); rc) return rc;
+            if (int rc = make_map(&bw, b_hi, N, K, ldb, true, pair ? PBN / 2 : PBN); rc) return rc;
+        if (pair) {
+            constexpr size_t smem = PCfg<2>::kSmem;
+            if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel<2>, d->device, (int)smem); rc)
+                return rc;
+            const uint64_t tiles = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
+            const unsigned grid = 2 * (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms / 2);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(PThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = d->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2>, a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K,
+                                       e, lay));
+            return SYNK_OK;
+        }
+        constexpr size_t smem = PCfg<1>::kSmem;
+        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel<1>, d->device, (int)smem); rc)
+            return rc;
         const uint64_t tiles = ((M + BM - 1) / BM) * ((N + PBN - 1) / PBN);
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
-        gemm_tc_persistent_kernel<<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K, e,
-                                                                         lay);
+        gemm_tc_persistent_kernel<1><<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N,
+                                                                            (uint32_t)K, e, lay);
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
         return SYNK_OK;
     }

@@ -574,7 +574,9 @@ __global__ void __launch_bounds__(256) ones_rows_kernel(OnesRows rows, uint64_t 
 struct Bf16Plan {
     uint64_t n, maxd, L;
     uint64_t off_w[64], off_wt[64], off_act[65], off_actT[65];
-    uint64_t off_pred, off_delta_f, off_d[2], off_dT, off_partial, total;
+    // off_d[k] (k = 1..L): delta at layer k-1's output, n x pad8(d_k) bf16;
+    // off_dT[k]: its transpose, for narrow layers (d_k <= kWideN) only
+    uint64_t off_pred, off_delta_f, off_d[65], off_dT[65], off_partial, total;
 };
 
 Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t maxd) {
@@ -588,13 +590,9 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
         at += (bytes + 255) / 256 * 256;
         return o;
     };
-    uint64_t narrow = 0;  // widest output dimension <= kWideN (needs W^T and delta^T)
     for (uint32_t l = 0; l < L; ++l) {
         p.off_w[l] = take(dims[l] * pad8(dims[l + 1]) * 2);
-        if (dims[l + 1] <= kWideN) {
-            p.off_wt[l] = take(dims[l + 1] * pad8(dims[l]) * 2);
-            narrow = std::max<uint64_t>(narrow, dims[l + 1]);
-        }
+        if (dims[l + 1] <= kWideN) p.off_wt[l] = take(dims[l + 1] * pad8(dims[l]) * 2);
     }
     for (uint32_t l = 0; l < L; ++l) {  // act[0] = x, act[l] hidden
         p.off_act[l] = take(n * pad8(dims[l]) * 2);
@@ -602,8 +600,10 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
     }
     p.off_pred = take(n * dims[L] * 4);
     p.off_delta_f = take(n * dims[L] * 4);
-    for (int i = 0; i < 2; ++i) p.off_d[i] = take(n * pad8(maxd) * 2);
-    p.off_dT = take(std::max<uint64_t>(narrow, 1) * pad8(n) * 2);
+    for (uint32_t k = 1; k <= L; ++k) {  // every delta stays live: all dX products run before the weight gradients
+        p.off_d[k] = take(n * pad8(dims[k]) * 2);
+        if (dims[k] <= kWideN) p.off_dT[k] = take(dims[k] * pad8(n) * 2);
+    }
     p.off_partial = take(kLossBlocks * sizeof(double));
     p.total = at;
     return p;
@@ -688,6 +688,8 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         OnesRows o{};
         o.count = L;
         for (uint32_t l = 0; l < L; ++l) o.p[l] = bf(B.off_actT[l]) + dims[l] * pad8(n);
+        if (int rc = synk::prefer_shared_carveout((const void*)ones_rows_kernel, d->device); rc) return rc;
+        if (int rc = synk::prefer_shared_carveout((const void*)loss_delta_kernel<float>, d->device); rc) return rc;
         ones_rows_kernel<<<dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 64), L), 256, 0, d->stream>>>(o, n);
         SYNK_LAUNCHED("ones_rows_kernel");
     }
@@ -718,44 +720,47 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
                                                                  reinterpret_cast<unsigned*>(d->flags_dev + 3),
                                                                  0.5 * inv_n, loss, rows, dl);
     SYNK_LAUNCHED("loss_delta_kernel");
-    int cur = 0;
-    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[cur]), pad8(P.maxd),
-                                      wide(L - 1) ? nullptr : bf(B.off_dT), pad8(n));
+    auto narrow = [&](uint32_t k) { return dims[k] <= kWideN; };  // delta_k also needed transposed
+    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[L]), pad8(dims[L]),
+                                      narrow(L) ? bf(B.off_dT[L]) : nullptr, pad8(n));
         rc)
         return rc;
 
-    // backward
-    for (uint32_t l = L; l-- > 0;) {
+    // backward: every dX product first (they read the bf16 W_l, which no
+    // update of this step touches), then the weight gradients, largest
+    // segment first: each segment's all-reduce + update (the trainer's second
+    // stream) then overlaps the remaining weight-gradient products and only
+    // the smallest one's is exposed at the end of the step (C5: the 8.4M-
+    // parameter W_0 update used to trail the last GEMM).
+    for (uint32_t l = L - 1; l >= 1; --l) {
+        // delta_l = (delta_{l+1} . W_l^T) * (1 - a_l^2)  (M = n, N = d_l, K = d_{l+1})
+        if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, dims[l], dims[l + 1], bf(B.off_d[l + 1]), nullptr,
+                                   pad8(dims[l + 1]), wbuf(l), nullptr, pad8(dims[l + 1]), 0, SYNK_EPI_TANH_GRAD, BF,
+                                   bf(B.off_d[l]), pad8(dims[l]), narrow(l) ? (void*)bf(B.off_dT[l]) : nullptr,
+                                   pad8(n), nullptr, bf(B.off_act[l]), pad8(dims[l]));
+            rc)
+            return rc;
+    }
+    uint32_t order[64];
+    for (uint32_t i = 0; i < L; ++i) order[i] = L - 1 - i;
+    std::stable_sort(order, order + L, [&](uint32_t a, uint32_t b) {
+        return dims[a] * dims[a + 1] > dims[b] * dims[b + 1];
+    });
+    for (uint32_t i = 0; i < L; ++i) {
+        const uint32_t l = order[i];
         const uint64_t din = dims[l], dout = dims[l + 1];
-        // [gW_l; gb_l] = [a_l^T; 1] . delta  (M = din + 1: the last row is the bias gradient)
-        const void* b = wide(l) ? (const void*)bf(B.off_d[cur]) : (const void*)bf(B.off_dT);
+        // [gW_l; gb_l] = [a_l^T; 1] . delta_{l+1}  (M = din + 1: the last row is the bias gradient)
+        const void* b = wide(l) ? (const void*)bf(B.off_d[l + 1]) : (const void*)bf(B.off_dT[l + 1]);
         if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, din + 1, dout, n, bf(B.off_actT[l]), nullptr, pad8(n), b,
-                                   nullptr, wide(l) ? pad8(P.maxd) : pad8(n), wide(l) ? SYNK_GEMM_B_MN : 0,
+                                   nullptr, wide(l) ? pad8(dout) : pad8(n), wide(l) ? SYNK_GEMM_B_MN : 0,
                                    SYNK_EPI_STORE, F32, grad + P.woff[l], dout, nullptr, 0, nullptr, nullptr, 0);
             rc)
             return rc;
-        // Segment [W_l, b_l] of the gradient is final, and the f32 W_l/b_l are
-        // not read again in this pass (the GEMMs read the bf16 copies made at
-        // the start): the trainer may all-reduce + update it from here on --
-        // unless the bf16 copy is the rank's shadow and that update rewrites
-        // it in place (no spare): then only after dX_l below has read W_l.
-        const bool late = shb && !opts->shadow_spare;
-        if (signal_base >= 0 && (!late || l == 0))
+        // Segment [W_l, b_l] of the gradient is final and W_l is not read again
+        // (every dX ran above): the trainer may all-reduce + update it now.
+        if (signal_base >= 0)
             if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
-        if (l > 0) {
-            // delta_prev = (delta . W_l^T) * (1 - a_l^2)  (M = n, N = din, K = dout)
-            const int nxt = cur ^ 1;
-            const bool narrow_prev = !wide(l - 1);  // gW_{l-1} then wants delta_prev^T
-            if (int rc = synk_gemm_tc2(d, SYNK_GEMM_BF16, n, din, dout, bf(B.off_d[cur]), nullptr, pad8(P.maxd),
-                                       wbuf(l), nullptr, pad8(dout), 0, SYNK_EPI_TANH_GRAD, BF, bf(B.off_d[nxt]),
-                                       pad8(P.maxd), narrow_prev ? (void*)bf(B.off_dT) : nullptr, pad8(n), nullptr,
-                                       bf(B.off_act[l]), pad8(din));
-                rc)
-                return rc;
-            cur = nxt;
-            if (signal_base >= 0 && late)
-                if (int rc = synk_signal_slot(d, signal_base + (int)l); rc) return rc;
-        }
+        if (opts && opts->seg_order) opts->seg_order[i] = (int)l;
     }
     return SYNK_OK;
 }

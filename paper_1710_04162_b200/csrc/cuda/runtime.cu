@@ -42,6 +42,22 @@ int ensure_max_smem(const void* kernel, int device, int bytes) {
     return SYNK_OK;
 }
 
+// Run `kernel` with the largest shared-memory carveout even if it uses no
+// shared memory itself. An SM switches its L1/shared split only once it has
+// drained, so a small kernel launched beside the persistent GEMMs (the
+// trainer's overlapped segment updates, the step's staging kernels) on the
+// default carveout keeps the next max-smem GEMM CTA off that SM until it
+// finishes (C5: 35 us before the narrow weight-gradient GEMM could start).
+int prefer_shared_carveout(const void* kernel, int device) {
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    if (done.count({kernel, device})) return SYNK_OK;
+    SYNK_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared));
+    done.insert({kernel, device});
+    return SYNK_OK;
+}
+
 static std::mutex g_pool_mutex;
 static std::set<int> g_pools_configured;
 
@@ -125,7 +141,13 @@ int synk_open(int world, const int* device_ids, synk_dev** out) {
         d->device = device_ids[r];
         SYNK_CU(cudaSetDevice(d->device));
         SYNK_CU(cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, d->device));
-        SYNK_CU(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        // Rank streams at the highest priority, the overlapped-collective
+        // (aux) streams at the lowest: pending CTAs of the rank's next GEMM are
+        // dispatched ahead of the remaining CTAs of an overlapped update, which
+        // only fills the SM room the GEMMs leave.
+        int least = 0, greatest = 0;
+        SYNK_CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SYNK_CU(cudaStreamCreateWithPriority(&d->stream, cudaStreamNonBlocking, greatest));
         SYNK_CU(cudaMalloc(&d->flags_dev, 4 * sizeof(int)));
         SYNK_CU(cudaMemset(d->flags_dev, 0, 4 * sizeof(int)));
         SYNK_CU(cudaHostAlloc(&d->flags_host, 4 * sizeof(int), cudaHostAllocPortable));
@@ -268,7 +290,9 @@ int synk_open_aux(synk_dev* main, synk_dev** out) {
     d->rank = main->rank;
     d->device = main->device;
     d->num_sms = main->num_sms;
-    cudaError_t e = cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking);
+    int least = 0, greatest = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&d->stream, cudaStreamNonBlocking, least);  // see synk_open
     if (e == cudaSuccess) e = cudaMalloc(&d->flags_dev, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(d->flags_dev, 0, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaHostAlloc(&d->flags_host, 4 * sizeof(int), cudaHostAllocPortable);

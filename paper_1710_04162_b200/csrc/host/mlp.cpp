@@ -136,6 +136,9 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     const bool shadowed = pvar && compute == MlpCompute::Bf16TensorCore;
     if (shadowed) opts.shadow = weight_shadow(*pvar, rd, params, c.dims, &opts.shadow_valid);
     opts.shadow_spare = opts.shadow != nullptr;  // a trainer update writes buf[cur ^ 1]
+    std::vector<int> seg_order(L);
+    for (std::uint32_t i = 0; i < L; ++i) seg_order[i] = static_cast<int>(L - 1 - i);  // backward order by default
+    opts.seg_order = seg_order.data();
     int signalled = 0;
     detail::check(synk_mlp_loss_grad_opts(rd->h, detail::synk_dtype(dt), mode, c.dims.data(), L, params.data(),
                                           xd.data(), yd.data(), c.n, static_cast<double*>(loss.data()), grad.data(), ws,
@@ -143,8 +146,8 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
                   "mlp_loss_grad");
     if (opts.shadow) mark_shadow_current(*pvar, rd->rank, params);
     if (signalled > 0) {
-        // Layer l's segment [W_l, b_l] was signalled on slot base + l, in
-        // backward order (l = L-1 ... 0); W_l and b_l are adjacent in the layout.
+        // Layer l's segment [W_l, b_l] was signalled on slot base + l, in the
+        // order the kernel reports (seg_order); W_l and b_l are adjacent in the layout.
         std::size_t at = 0;
         std::vector<std::size_t> first(L), count(L);
         for (std::uint32_t l = 0; l < L; ++l) {
@@ -152,7 +155,10 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
             count[l] = c.dims[l] * c.dims[l + 1] + c.dims[l + 1];
             at += count[l];
         }
-        for (std::uint32_t l = L; l-- > 0;) ctx->grad_segments->push_back({first[l], count[l], base + int(l)});
+        for (std::uint32_t i = 0; i < L; ++i) {
+            const std::uint32_t l = static_cast<std::uint32_t>(seg_order[i]);
+            ctx->grad_segments->push_back({first[l], count[l], base + int(l)});
+        }
     }
     return {loss, grad};
 }
