@@ -29,12 +29,12 @@ using synk::combine_op;
 
 constexpr int kMaxWorld = 64;
 constexpr int kBlock = 256;
-// The fused all-reduce + update runs beside the persistent GEMM (overlapped
-// segment updates): 384 GEMM threads x 128 registers leave 16K registers per
-// SM, so 128-thread CTAs (74 registers) can co-reside and start as soon as
-// their segment is final; 256-thread CTAs could not, and waited for GEMM CTAs
-// to retire (C5: the W_1 update started 60 us into the next GEMM).
-constexpr int kStepBlock = 128;
+// The fused all-reduce + update: 256-thread CTAs, 4 per SM, one vector item
+// per thread per iteration (74 registers). Measured against 128-thread CTAs
+// that co-reside with the persistent GEMM and two items in flight per thread
+// (122 registers): C5 1.053 vs 1.065-1.075 ms (serialised or overlapped), so
+// the occupancy of the streaming loop matters more than co-residency.
+constexpr int kStepBlock = 256;
 
 struct Ptrs {
     void* p[kMaxWorld];
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kStepBlock) allreduce_step_kernel(
     if constexpr (W > 0) {
         if (vec_bytes && coherent) {
             // lo is 16-element aligned, so a multiple of both vector widths
-            constexpr int U = W <= 2 ? 2 : 1;  // items in flight per thread (registers: W + 3 vectors each)
+            constexpr int U = 1;  // items per thread per iteration (2: fewer CTAs resident, slower)
             if (vec_bytes == 32) {
                 constexpr int N = VecT<T, 32>::N;
                 const uint64_t v0 = lo / N, v1 = hi / N;
@@ -517,7 +517,7 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
     const uint64_t items = vec_bytes ? (hi - lo) / (vec_bytes / sizeof(T)) + 1 : hi - lo;
     // at most 4 CTAs per SM (37K registers): beside them the next narrow GEMM
     // still fits its two CTAs per SM (94 registers x 128 threads each)
-    unsigned grid = synk::grid_for(d, items, kStepBlock, 8);
+    unsigned grid = synk::grid_for(d, items, kStepBlock);
     if (flags & SYNK_STEP_BACKGROUND) {
         // Overlapped with tensor-core GEMMs on the other stream: a few CTAs
         // stream the segment at a fraction of HBM bandwidth instead of

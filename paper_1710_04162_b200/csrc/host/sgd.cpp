@@ -332,7 +332,15 @@ double SyncSgd::fused_step(const ParallelFunction& f_grad, const std::vector<Fun
             detail::check(synk_signal(rd->h), "signal");
             rv.arrive_and_wait();
         }
-        bool overlap = !unequal;
+        // SYNK_STEP_OVERLAP: 1 overlaps the segment updates with the backward
+        // GEMMs at every world size, 0 never; unset: only when W > 1 (there is
+        // an NVLink transfer to hide). On one GPU the update is pure HBM work
+        // that competes with the GEMMs for SM slots.
+        static const int overlap_mode = [] {
+            const char* e = std::getenv("SYNK_STEP_OVERLAP");
+            return e ? std::atoi(e) : -1;
+        }();
+        bool overlap = !unequal && (overlap_mode == 1 || (overlap_mode == -1 && W > 1));
         for (std::size_t p = 0; p < W; ++p) overlap = overlap && seg_cover[p] && seg_counts[p] == segs.size();
         // bf16 weight shadows (the bf16 MLP's operand copies, one per rank):
         // when every rank holds a current one, the update writes them along
