@@ -267,7 +267,7 @@ __device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t g
 // of one dependent round trip per array -- the update runs beside the
 // persistent GEMMs with one 128-thread CTA per SM, where memory-level
 // parallelism per thread sets its bandwidth.
-template <class T, int W, int BYTES, bool SH, int U>
+template <class T, int W, int BYTES, bool SH, int U, int RULE>
 __device__ __forceinline__ void step_vectors(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
                                              int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
                                              int naux, uint64_t v0, uint64_t vstride, uint64_t v_end, const Shadow& sh,
@@ -311,7 +311,7 @@ __device__ __forceinline__ void step_vectors(const Ptrs& params, const Ptrs& gra
             double pd = (double)pn.e[k];
             double d0 = (double)x0.e[k];
             double d1 = (double)x1.e[k];
-            synk::rule_update(rp, pd, d0, d1, (double)g.e[k]);
+            synk::rule_update_t<RULE>(rp, pd, d0, d1, (double)g.e[k]);
             pn.e[k] = (T)pd;
             x0.e[k] = (T)d0;
             x1.e[k] = (T)d1;
@@ -326,6 +326,29 @@ __device__ __forceinline__ void step_vectors(const Ptrs& params, const Ptrs& gra
     }
 }
 
+// The vector part of one rank's chunk [lo, hi): returns where the scalar
+// tail starts.
+template <class T, int W, bool SH, int RULE>
+__device__ __forceinline__ uint64_t vector_loop(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
+                                                int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
+                                                int naux, uint64_t lo, uint64_t hi, uint64_t tid, uint64_t stride,
+                                                int vec_bytes, const Shadow& sh, bool grads_local) {
+    if (vec_bytes == 32) {
+        constexpr int N = VecT<T, 32>::N;
+        const uint64_t v0 = lo / N, v1 = hi / N;
+        for (uint64_t v = v0 + tid; v < v1; v += stride)
+            step_vectors<T, W, 32, SH, 1, RULE>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v,
+                                                stride, v1, sh, grads_local);
+        return v1 * N;
+    }
+    constexpr int N = VecT<T, 16>::N;
+    const uint64_t v0 = lo / N, v1 = hi / N;
+    for (uint64_t v = v0 + tid; v < v1; v += stride)
+        step_vectors<T, W, 16, SH, 1, RULE>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v, stride,
+                                            v1, sh, grads_local);
+    return v1 * N;
+}
+
 template <class T, int W, bool SH>
 __global__ void __launch_bounds__(kStepBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
@@ -336,22 +359,20 @@ __global__ void __launch_bounds__(kStepBlock) allreduce_step_kernel(
     uint64_t stride = (uint64_t)gridDim.x * kStepBlock;
     if constexpr (W > 0) {
         if (vec_bytes && coherent) {
-            // lo is 16-element aligned, so a multiple of both vector widths
-            constexpr int U = 1;  // items per thread per iteration (2: fewer CTAs resident, slower)
-            if (vec_bytes == 32) {
-                constexpr int N = VecT<T, 32>::N;
-                const uint64_t v0 = lo / N, v1 = hi / N;
-                for (uint64_t v = v0 + tid; v < v1; v += stride * U)
-                    step_vectors<T, W, 32, SH, U>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v,
-                                                  stride, v1, sh, grads_local);
-                lo = v1 * N;  // scalar tail below
-            } else {
-                constexpr int N = VecT<T, 16>::N;
-                const uint64_t v0 = lo / N, v1 = hi / N;
-                for (uint64_t v = v0 + tid; v < v1; v += stride * U)
-                    step_vectors<T, W, 16, SH, U>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, v,
-                                                  stride, v1, sh, grads_local);
-                lo = v1 * N;
+            // lo is 16-element aligned, so a multiple of both vector widths;
+            // one loop per rule, each with that rule's code only
+            switch (rp.rule) {
+            case SYNK_RULE_SGD:
+                lo = vector_loop<T, W, SH, SYNK_RULE_SGD>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp,
+                                                          naux, lo, hi, tid, stride, vec_bytes, sh, grads_local);
+                break;
+            case SYNK_RULE_MOMENTUM:
+                lo = vector_loop<T, W, SH, SYNK_RULE_MOMENTUM>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp,
+                                                               naux, lo, hi, tid, stride, vec_bytes, sh, grads_local);
+                break;
+            default:
+                lo = vector_loop<T, W, SH, -1>(params, grads, aux0, aux1, rank, grad_op, fop, inv_w, rp, naux, lo, hi,
+                                               tid, stride, vec_bytes, sh, grads_local);
             }
         }
     }

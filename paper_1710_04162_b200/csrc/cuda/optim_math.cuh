@@ -47,6 +47,23 @@ __device__ __forceinline__ void rule_update(const RuleParams& rp, double& p, dou
     }
 }
 
+// The same with the rule fixed at compile time (RULE < 0: rp.rule at run
+// time): the streaming update loop then carries one rule's code only.
+template <int RULE>
+__device__ __forceinline__ void rule_update_t(const RuleParams& rp, double& p, double& a0, double& a1, double g) {
+    if constexpr (RULE < 0) {
+        rule_update(rp, p, a0, a1, g);
+    } else {
+        RuleParams r = rp;
+        r.rule = RULE;
+        if constexpr (RULE == SYNK_RULE_SGD) {
+            p = __dsub_rn(p, __dmul_rn(rp.lr, g));
+        } else {
+            rule_update(r, p, a0, a1, g);  // switch folds: r.rule is a constant
+        }
+    }
+}
+
 inline int rule_aux_count(int rule) {
     return rule == SYNK_RULE_SGD ? 0 : (rule == SYNK_RULE_ADAM ? 2 : 1);
 }
