@@ -78,7 +78,7 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-TRAFFIC_CAPTURE = "profiles/r01_gather_ncu_full_raw.csv"
+TRAFFIC_CAPTURE = "profiles/r02_gather_ncu_full_raw.csv"
 
 
 def ncu_traffic(bytes_per_launch, path=TRAFFIC_CAPTURE):
@@ -499,9 +499,10 @@ SGD_MODELS = {
                     "SGD lr 0.01, gradient all-reduce mean fused with the update"},
     "c5": {"dims": [2048, 4096, 4096, 100], "per_gpu": 8192, "rows": 16384, "compute": "bf16", "warm": 3,
            "dtype": "bf16",
-           "label": "C5 (R1): MLP 2048-4096-4096-100 (25,583,716 params, fp32 master), bf16 tcgen05 GEMMs, indexed "
-                    "from a 16384-row HBM mirror, SGD lr 0.01, gradient all-reduce mean + update fused and bucketed "
-                    "per layer (overlapped with the backward pass)"},
+           "label": "C5 (R1): MLP 2048-4096-4096-100 (25,583,716 params, fp32 master), bf16 tcgen05 GEMMs "
+                    "(CTA-pair 256x256 tiles for the wide layers), indexed from a 16384-row HBM mirror, SGD lr 0.01, "
+                    "gradient all-reduce mean + update fused; at W > 1 bucketed per layer and overlapped with the "
+                    "backward pass, at W = 1 one update after it"},
 }
 
 
@@ -818,9 +819,10 @@ def sync_sgd_section(sk, args, n_gpus, model, dry=False):
            "table1_note": "function = gradient-call compute (mean over ranks, device events); shuffle = staging of "
                           "the indexed batch before compute (0 when the gather is fused into the compute graph); "
                           "straggler = max - mean rank task; allreduce = the fused all-reduce + 1/W + update "
-                          "kernel (so the update sits here, not in function); for C5 the all-reduce + update runs "
-                          "per layer on a second stream, overlapped with the backward GEMMs, so its span overlaps "
-                          "function and the parts sum to more than total"}
+                          "kernel (so the update sits here, not in function); for C5 at W > 1 the all-reduce + "
+                          "update runs per layer on a second stream, overlapped with the backward GEMMs, so its "
+                          "span overlaps function and the parts sum to more than total (at W = 1 it follows the "
+                          "backward pass)"}
     if model == "c5":
         bf16_peak, bf16_sustained, peak_kind = 1609.7, 1365.0, "fallback"
         try:
