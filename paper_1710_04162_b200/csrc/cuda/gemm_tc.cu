@@ -968,22 +968,30 @@ __global__ void __launch_bounds__(256) prep2_bf16_kernel(const float* __restrict
     if (t < 64) srow[t] = r0 + t < rows ? (rowmap ? rowmap[r0 + t] : r0 + t) : 0;
     __syncthreads();
     const int lc = (t % 16) * 4;  // 4 consecutive columns
+    // all four passes' loads issued before the first use (4 x 16 B in flight per thread)
+    float vv[4][4];
 #pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
         const int lr = t / 16 + 16 * pass;
         const uint64_t r = r0 + lr, c = c0 + lc;
         const uint64_t ri = srow[lr];
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        vv[pass][0] = vv[pass][1] = vv[pass][2] = vv[pass][3] = 0.f;
         if (r < rows) {
             if (vec_in && c + 4 <= cols) {
                 const float4 f = __ldcs(reinterpret_cast<const float4*>(in + ri * ld_in + c));
-                v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+                vv[pass][0] = f.x, vv[pass][1] = f.y, vv[pass][2] = f.z, vv[pass][3] = f.w;
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (c + j < cols) v[j] = in[ri * ld_in + c + j];
+                    if (c + j < cols) vv[pass][j] = in[ri * ld_in + c + j];
             }
         }
+    }
+#pragma unroll
+    for (int pass = 0; pass < 4; ++pass) {
+        const int lr = t / 16 + 16 * pass;
+        const uint64_t r = r0 + lr, c = c0 + lc;
+        const float* v = vv[pass];
 #pragma unroll
         for (int j = 0; j < 4; ++j) tile[lr][lc + j] = v[j];
         if (out && r < rows) {

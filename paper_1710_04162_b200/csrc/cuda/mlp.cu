@@ -571,6 +571,85 @@ __global__ void __launch_bounds__(256) ones_rows_kernel(OnesRows rows, uint64_t 
             rows.p[l][i] = one;
 }
 
+// Loss + output delta for the bf16 path in one launch, tiled 32 rows x 64
+// columns per CTA: diff = pred - y (f64, y read through the index list when
+// index-fused), loss partial sum (f64; the last CTA folds the per-CTA
+// partials in a fixed order), delta = (float)(diff * inv_n) written straight
+// in its bf16 operand forms -- row-major (ld) and, for a narrow output layer,
+// transposed through a shared-memory tile (ldt) -- so neither the f32 delta
+// nor the separate cast + transpose launch exists. Same per-element rounding
+// as loss_delta_kernel + the cast (f64 -> f32 -> bf16).
+constexpr int kLossTileR = 32, kLossTileC = 64;
+__global__ void __launch_bounds__(256) loss_delta_bf16_kernel(const float* __restrict__ pred, const float* __restrict__ y,
+                                                              uint64_t n, uint64_t cols, double inv_n,
+                                                              __nv_bfloat16* __restrict__ d, uint64_t ld,
+                                                              __nv_bfloat16* __restrict__ dt, uint64_t ldt,
+                                                              double* __restrict__ partial, unsigned* __restrict__ counter,
+                                                              double scale, double* __restrict__ loss,
+                                                              const uint64_t* __restrict__ yrows) {
+    __shared__ __nv_bfloat16 tile[kLossTileC][kLossTileR + 2];
+    __shared__ double red[256];
+    __shared__ int last;
+    const uint64_t r0 = (uint64_t)blockIdx.y * kLossTileR, c0 = (uint64_t)blockIdx.x * kLossTileC;
+    const int tc = threadIdx.x % kLossTileC, tr = threadIdx.x / kLossTileC;  // 64 x 4
+    double s = 0.0;
+#pragma unroll
+    for (int k = tr; k < kLossTileR; k += 4) {
+        const uint64_t r = r0 + k, c = c0 + tc;
+        __nv_bfloat16 h = __float2bfloat16_rn(0.f);
+        if (r < n && c < cols) {
+            const uint64_t yr = yrows ? __ldg(yrows + r) : r;
+            const double diff = __dsub_rn((double)pred[r * cols + c], (double)y[yr * cols + c]);
+            s = __dadd_rn(s, __dmul_rn(diff, diff));
+            h = __float2bfloat16_rn((float)__dmul_rn(diff, inv_n));
+            d[r * ld + c] = h;
+        }
+        tile[tc][k] = h;
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (dt) {  // transposed: thread -> (column c0 + t / 4, rows r0 + (t % 4) * 8 .. + 8)
+        const int oc = threadIdx.x / 4, seg = (threadIdx.x % 4) * 8;
+        const uint64_t c = c0 + oc;
+        if (c < cols) {
+            if (r0 + seg + 8 <= n) {  // 8 consecutive rows = one 16-byte store (ldt is a multiple of 8)
+                __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[j] = tile[oc][seg + j];
+                *reinterpret_cast<uint4*>(dt + c * ldt + r0 + seg) = *reinterpret_cast<const uint4*>(h);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (r0 + seg + j < n) dt[c * ldt + r0 + seg + j] = tile[oc][seg + j];
+            }
+        }
+    }
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const unsigned nb = gridDim.x * gridDim.y, b = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) partial[b] = red[0];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == nb - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (unsigned i = threadIdx.x; i < nb; i += 256) t += __ldcg(&partial[i]);
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *loss = red[0] * scale;  // mlp.cpp:190: loss *= 0.5 * inv_n
+        *counter = 0;
+    }
+}
+
 struct Bf16Plan {
     uint64_t n, maxd, L;
     uint64_t off_w[64], off_wt[64], off_act[65], off_actT[65];
@@ -604,7 +683,7 @@ Bf16Plan make_bf16_plan(const uint64_t* dims, uint32_t L, uint64_t n, uint64_t m
         p.off_d[k] = take(n * pad8(dims[k]) * 2);
         if (dims[k] <= kWideN) p.off_dT[k] = take(dims[k] * pad8(n) * 2);
     }
-    p.off_partial = take(kLossBlocks * sizeof(double));
+    p.off_partial = take(kLossBlocks * 8 * sizeof(double));  // loss tiles (loss_delta_bf16_kernel)
     p.total = at;
     return p;
 }
@@ -710,21 +789,20 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
 
     // loss + output delta (f32), then its bf16 operand form(s)
     const uint64_t dl = dims[L], n_el = n * dl;
-    float* delta_f = reinterpret_cast<float*>(base + B.off_delta_f);
     double* partial = reinterpret_cast<double*>(base + B.off_partial);
-    int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
     const double inv_n = 1.0 / (double)n;
     if (rows)
         if (int rc = wait_rows(); rc) return rc;  // the loss reads y through the staged list
-    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(pred, y, n_el, inv_n, delta_f, partial,
-                                                                 reinterpret_cast<unsigned*>(d->flags_dev + 3),
-                                                                 0.5 * inv_n, loss, rows, dl);
-    SYNK_LAUNCHED("loss_delta_kernel");
     auto narrow = [&](uint32_t k) { return dims[k] <= kWideN; };  // delta_k also needed transposed
-    if (int rc = synk_gemm_prep2_bf16(d, delta_f, n, dl, dl, bf(B.off_d[L]), pad8(dims[L]),
-                                      narrow(L) ? bf(B.off_dT[L]) : nullptr, pad8(n));
-        rc)
-        return rc;
+    {
+        const dim3 grid((unsigned)((dl + kLossTileC - 1) / kLossTileC), (unsigned)((n + kLossTileR - 1) / kLossTileR));
+        SYNK_REQUIRE((uint64_t)grid.x * grid.y <= kLossBlocks * 8, SYNK_EARG, "mlp: loss tile grid too large");
+        if (int rc = synk::prefer_shared_carveout((const void*)loss_delta_bf16_kernel, d->device); rc) return rc;
+        loss_delta_bf16_kernel<<<grid, 256, 0, d->stream>>>(
+            pred, y, n, dl, inv_n, bf(B.off_d[L]), pad8(dims[L]), narrow(L) ? bf(B.off_dT[L]) : nullptr, pad8(n),
+            partial, reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n, loss, rows);
+        SYNK_LAUNCHED("loss_delta_bf16_kernel");
+    }
 
     // backward: every dX product first (they read the bf16 W_l, which no
     // update of this step touches), then the weight gradients, largest
