@@ -233,6 +233,15 @@ __device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t g
     __nv_bfloat16* w = reinterpret_cast<__nv_bfloat16*>(b + g.off_w);
     __nv_bfloat16* wt = g.off_wt == SYNK_NO_TRANSPOSE ? nullptr : reinterpret_cast<__nv_bfloat16*>(b + g.off_wt);
     const uint64_t size = g.rows * g.cols;
+    if (N == 8 && !wt && g.ldw == g.cols && gi >= g.first && gi + 8 <= g.first + size && ((gi - g.first) & 7) == 0) {
+        // unpadded rows: the shadow is the segment itself, no row split (no
+        // 64-bit division per vector on the update's streaming path)
+        __nv_bfloat162 h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        *reinterpret_cast<uint4*>(w + (gi - g.first)) = *reinterpret_cast<const uint4*>(h);
+        return;
+    }
     if (N == 8 && gi >= g.first && gi + 8 <= g.first + size) {
         const uint64_t o = gi - g.first, r = o / g.cols, c = o - r * g.cols;
         const uint64_t at = r * g.ldw + c;
@@ -559,11 +568,15 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
         if (with) {                                                                                              \
             if (int rc = synk::prefer_shared_carveout((const void*)allreduce_step_kernel<T, WW, true>, d->device); rc) \
                 return rc;                                                                                       \
+            if (!(flags & SYNK_STEP_BACKGROUND))                                                                 \
+                grid = synk::resident_grid((const void*)allreduce_step_kernel<T, WW, true>, d->device, kStepBlock, items); \
             allreduce_step_kernel<T, WW, true><<<grid, kStepBlock, 0, d->stream>>>(                                  \
                 P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
         } else {                                                                                                 \
             if (int rc = synk::prefer_shared_carveout((const void*)allreduce_step_kernel<T, WW, false>, d->device); rc) \
                 return rc;                                                                                       \
+            if (!(flags & SYNK_STEP_BACKGROUND))                                                                 \
+                grid = synk::resident_grid((const void*)allreduce_step_kernel<T, WW, false>, d->device, kStepBlock, items); \
             allreduce_step_kernel<T, WW, false><<<grid, kStepBlock, 0, d->stream>>>(                                 \
                 P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
         }                                                                                                        \

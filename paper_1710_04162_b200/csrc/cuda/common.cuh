@@ -42,6 +42,8 @@ int ensure_max_smem(const void* kernel, int device, int bytes);
 // Largest shared-memory carveout for a kernel that runs beside max-smem GEMMs
 // (no SM reconfiguration drain between them); once per (kernel, device).
 int prefer_shared_carveout(const void* kernel, int device);
+// Grid that keeps every CTA of a grid-stride kernel resident at once.
+unsigned resident_grid(const void* kernel, int device, int block, uint64_t work_items);
 
 // Releases the rank's graph cache (mlp.cu); called by synk_close.
 void release_graphs(synk_dev* d);

@@ -7,6 +7,7 @@
 
 #include <stdio.h>
 
+#include <map>
 #include <mutex>
 #include <set>
 
@@ -56,6 +57,31 @@ int prefer_shared_carveout(const void* kernel, int device) {
                                  (int)cudaSharedmemCarveoutMaxShared));
     done.insert({kernel, device});
     return SYNK_OK;
+}
+
+// Grid for a grid-stride streaming kernel: every CTA resident at once (SMs x
+// CTAs per SM at this block size, from the occupancy calculator, cached per
+// (kernel, device)), never more than the work needs. A grid of several
+// partial waves leaves the last wave's CTAs streaming alone at the end.
+unsigned resident_grid(const void* kernel, int device, int block, uint64_t work_items) {
+    static std::map<std::pair<const void*, int>, int> occ;
+    int per_sm = 0, sms = 148;
+    {
+        std::lock_guard<std::mutex> lock(g_attr_mutex);
+        auto it = occ.find({kernel, device});
+        if (it == occ.end()) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1)
+                per_sm = 1;
+            occ[{kernel, device}] = per_sm;
+        } else {
+            per_sm = it->second;
+        }
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    uint64_t need = (work_items + block - 1) / block;
+    if (need < 1) need = 1;
+    const uint64_t cap = (uint64_t)sms * (uint64_t)per_sm;
+    return (unsigned)(need < cap ? need : cap);
 }
 
 static std::mutex g_pool_mutex;
