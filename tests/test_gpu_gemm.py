@@ -114,6 +114,22 @@ def test_bf16_persistent_many_tiles(M, N, K):
     np.testing.assert_array_equal(got_t, got.T)
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 136, 64), (129, 257, 100), (300, 520, 1000), (255, 130, 8), (513, 4100, 72)])
+def test_bf16_pair_kernel_ragged_edges(M, N, K):
+    """The CTA-pair (cta_group::2) persistent kernel on ragged shapes: a pair
+    tile whose odd CTA holds only out-of-range A rows (M <= 128), partial N
+    tiles, K below one block, more tiles than pairs with a ragged last round;
+    C and C^T against fp64 on bf16-exact inputs."""
+    rng = np.random.default_rng(M * 3 + N + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)))
+    want = a.astype(np.float64) @ b.astype(np.float64).T
+    with Ranks(1) as R:
+        got, got_t = gemm(R, "bf16", a, b, want_t=True)
+    assert rel_err(got, want) <= 1e-6 + 5e-8 * K
+    np.testing.assert_array_equal(got_t, got.T)
+
+
 def test_fused_epilogues():
     rng = np.random.default_rng(2)
     M, N, K = 192, 160, 256
