@@ -545,13 +545,21 @@ __device__ __forceinline__ void epi_chunk(const EpiArgs& epi, uint64_t m, uint64
 // barriers (multicast), and each CTA drains its own 128 accumulator rows from
 // its own TMEM; the leader's TMEM-empty barrier counts both CTAs' epilogue warps.
 constexpr int PBN = 256, PThreads = 384, PEpiThreads = 256;
-template <int PAIR>
+// ACT: the short-K tanh-derivative products (C5's dX with K = d_{l+1} <= 128)
+// are bound by the activation read of their epilogue, not by the tensor
+// cores: the producer TMA-stages each tile's 128 x 256 activation block into
+// one of two shared-memory buffers (SWIZZLE_128B, 64-column boxes) while the
+// epilogue drains the previous tile, instead of every epilogue thread loading
+// its 256 B from HBM after the previous tile's stores. Two operand stages
+// suffice for K <= 128.
+template <int PAIR, bool ACT = false>
 struct PCfg {
-    static constexpr int kStages = PAIR == 2 ? 6 : 4;
+    static constexpr int kStages = ACT ? 2 : (PAIR == 2 ? 6 : 4);
     static constexpr int kA = 128 * 128;                // bytes per stage: this CTA's 128 A rows
     static constexpr int kB = (PBN / PAIR) * 128;       // this CTA's B rows (256 or 128), 128 B each
     static constexpr int kTileM = 128 * PAIR;
-    static constexpr size_t kSmem = (size_t)kStages * (kA + kB) + 1024 + 256;
+    static constexpr int kActBuf = ACT ? 128 * PBN * 2 : 0;  // one activation tile (bf16)
+    static constexpr size_t kSmem = (size_t)kStages * (kA + kB) + 2 * (size_t)kActBuf + 1024 + 256;
 };
 constexpr int PStages = PCfg<1>::kStages;  // (1-CTA layout, host-side sizes)
 constexpr int PA = PCfg<1>::kA, PB = PCfg<1>::kB;
@@ -590,22 +598,26 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
         : "memory");
 }
 
-template <int PAIR>
+template <int PAIR, bool ACT>
 __global__ void __launch_bounds__(PThreads, 1)
     gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                              uint32_t M, uint32_t N, uint32_t K, EpiArgs epi, uint32_t layout) {
-    using PC = PCfg<PAIR>;
+                              const __grid_constant__ CUtensorMap tact, uint32_t M, uint32_t N, uint32_t K,
+                              EpiArgs epi, uint32_t layout) {
+    using PC = PCfg<PAIR, ACT>;
     constexpr int kStages = PC::kStages, kA = PC::kA, kB = PC::kB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sa = smem;
     uint8_t* sb = smem + kStages * kA;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + kStages * kB);
+    uint8_t* sact = sb + kStages * kB;  // [2][4 boxes of 128 rows x 128 B] (ACT only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sact + 2 * PC::kActBuf);
     uint64_t* full = bars;                 // [kStages]
     uint64_t* empty = bars + kStages;      // [kStages]
     uint64_t* tfull = bars + 2 * kStages;  // [2]
     uint64_t* tempty = tfull + 2;          // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* act_full = tempty + 2;       // [2] (ACT)
+    uint64_t* act_empty = act_full + 2;    // [2] (ACT)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_empty + 2);
     const uint32_t rank = PAIR == 2 ? cluster_rank() : 0u;
     const bool leader = rank == 0;
     const uint32_t unit = blockIdx.x / PAIR, units = gridDim.x / PAIR;  // pair (or CTA) index / count
@@ -625,10 +637,13 @@ __global__ void __launch_bounds__(PThreads, 1)
             mbar_init(smem_u32(&tfull[b]), 1);
             // every epilogue warp of the pair arrives (one elected lane each)
             mbar_init(smem_u32(&tempty[b]), PAIR * (PEpiThreads / 32));
+            mbar_init(smem_u32(&act_full[b]), 1);
+            mbar_init(smem_u32(&act_empty[b]), PEpiThreads / 32);  // this CTA's epilogue warps
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_map(&ta);
         prefetch_map(&tb);
+        if (ACT) prefetch_map(&tact);
     }
     __syncwarp();
     // the pair's TMEM allocation touches both SMs' allocator state: both CTAs
@@ -653,9 +668,18 @@ __global__ void __launch_bounds__(PThreads, 1)
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer (both CTAs: this CTA's A rows and B rows) ----
-        uint32_t it = 0;
-        for (uint32_t t = unit; t < tiles; t += units) {
+        uint32_t it = 0, tl = 0;
+        for (uint32_t t = unit; t < tiles; t += units, ++tl) {
             const int m0 = (int)((t / num_n) * PC::kTileM + rank * 128), n0 = (int)((t % num_n) * PBN + rank * (PBN / PAIR));
+            if constexpr (ACT) {  // this CTA's 128 x 256 activation tile, two tiles ahead at most
+                const uint32_t ab = tl & 1;
+                mbar_wait(smem_u32(&act_empty[ab]), ((tl >> 1) & 1) ^ 1);
+                mbar_expect_tx(smem_u32(&act_full[ab]), PC::kActBuf);
+#pragma unroll
+                for (int j = 0; j < PBN / 64; ++j)
+                    tma_load_2d(smem_u32(sact + ab * PC::kActBuf + j * 16384), &tact, smem_u32(&act_full[ab]),
+                                (int)((t % num_n) * PBN) + 64 * j, m0);
+            }
             for (int kb = 0; kb < num_kb; ++kb, ++it) {
                 const int s = it % kStages;
                 mbar_wait(smem_u32(&empty[s]), ((it / kStages) & 1) ^ 1);
@@ -737,6 +761,59 @@ __global__ void __launch_bounds__(PThreads, 1)
             const uint64_t m = m0 + quad * 32 + lane;
             const uint32_t base = tmem + acc * PBN + ((uint32_t)(quad * 32) << 16);
             const int cbeg = half * (PBN / 2), cend = cbeg + PBN / 2;
+            if constexpr (ACT) {
+                const uint32_t ab = tl & 1;
+                mbar_wait(smem_u32(&act_full[ab]), (tl >> 1) & 1);
+                mbar_wait(smem_u32(&tfull[acc]), (tl >> 1) & 1);
+                tc_fence_after();
+                const int rl = quad * 32 + lane;  // row within this CTA's 128
+                const uint32_t abase = smem_u32(sact + ab * PC::kActBuf) + rl * 128;
+                const bool row = m < M;
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k) {
+                    uint32_t r[16];
+                    tmem_ld16(base + cbeg + 16 * k, r);
+                    const int c = cbeg + 16 * k;          // tile column of the chunk
+                    const uint32_t u = (uint32_t)(c % 64) / 8;  // 16-byte unit within the 128-byte row
+                    const uint32_t box = abase + (uint32_t)(c / 64) * 16384;
+                    uint4 a0, a1;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(a0.x), "=r"(a0.y), "=r"(a0.z), "=r"(a0.w)
+                                 : "r"(box + ((u ^ (rl & 7)) << 4)));
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(a1.x), "=r"(a1.y), "=r"(a1.z), "=r"(a1.w)
+                                 : "r"(box + (((u + 1) ^ (rl & 7)) << 4)));
+                    if (!row || n0 + c >= N) continue;
+                    if (c32 && n0 + c + 16 <= N) {
+                        const __nv_bfloat16* h0 = reinterpret_cast<const __nv_bfloat16*>(&a0);
+                        const __nv_bfloat16* h1 = reinterpret_cast<const __nv_bfloat16*>(&a1);
+                        uint32_t w[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float x0 = __bfloat162float(j < 4 ? h0[2 * j] : h1[2 * j - 8]);
+                            const float x1 = __bfloat162float(j < 4 ? h0[2 * j + 1] : h1[2 * j - 7]);
+                            const float v0 = __uint_as_float(r[2 * j]) * (1.0f - x0 * x0);
+                            const float v1 = __uint_as_float(r[2 * j + 1]) * (1.0f - x1 * x1);
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(v0, v1);
+                            w[j] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                        st256(static_cast<__nv_bfloat16*>(epi.c) + m * epi.ldc + n0 + c, w);
+                        if (epi.ct) {
+                            __nv_bfloat16* col = static_cast<__nv_bfloat16*>(epi.ct) + (n0 + c) * epi.ldct + m;
+                            const __nv_bfloat16* hw = reinterpret_cast<const __nv_bfloat16*>(w);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j, col += epi.ldct) *col = hw[j];
+                        }
+                    } else {
+                        epi_chunk(epi, m, n0 + c, N, r, vec_c, vec_act, true, a0, a1);
+                    }
+                }
+                // this warp is done with the activation buffer and the accumulator
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&act_empty[ab])) : "memory");
+                drained(acc);
+                continue;
+            }
             if (pre_ok && n0 + cend <= N) {  // warp-uniform: tcgen05.ld is .sync.aligned
                 // tanh-derivative epilogue, whole half-row inside the matrix:
                 // the thread's 128 activations (256 B, 16 loads) are issued
@@ -1149,9 +1226,17 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         if (!(lay & kBMn))
             if (int rc = make_map(&bw, b_hi, N, K, ldb, true, pair ? PBN / 2 : PBN); rc) return rc;
         if (pair) {
-            constexpr size_t smem = PCfg<2>::kSmem;
-            if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel<2>, d->device, (int)smem); rc)
-                return rc;
+            // short-K tanh-derivative product with a 16-byte aligned bf16 activation:
+            // the activation tiles are TMA-staged (PCfg ACT)
+            const bool act_tma = epilogue == SYNK_EPI_TANH_GRAD && out_dtype == 3 && K <= 128 && act &&
+                                 (reinterpret_cast<uintptr_t>(act) & 15) == 0 && (ldact * 2) % 16 == 0;
+            CUtensorMap ta = bw;
+            if (act_tma)
+                if (int rc = make_map(&ta, act, M, N, ldact, true, 128); rc) return rc;
+            const void* kern = act_tma ? (const void*)gemm_tc_persistent_kernel<2, true>
+                                       : (const void*)gemm_tc_persistent_kernel<2, false>;
+            const size_t smem = act_tma ? PCfg<2, true>::kSmem : PCfg<2, false>::kSmem;
+            if (int rc = synk::ensure_max_smem(kern, d->device, (int)smem); rc) return rc;
             const uint64_t tiles = ((M + 255) / 256) * ((N + PBN - 1) / PBN);
             const unsigned grid = 2 * (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms / 2);
             cudaLaunchConfig_t cfg = {};
@@ -1166,17 +1251,21 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2>, a0, bw, (uint32_t)M, (uint32_t)N, (uint32_t)K,
-                                       e, lay));
+            if (act_tma)
+                SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2, true>, a0, bw, ta, (uint32_t)M,
+                                           (uint32_t)N, (uint32_t)K, e, lay));
+            else
+                SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2, false>, a0, bw, ta, (uint32_t)M,
+                                           (uint32_t)N, (uint32_t)K, e, lay));
             return SYNK_OK;
         }
         constexpr size_t smem = PCfg<1>::kSmem;
-        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel<1>, d->device, (int)smem); rc)
+        if (int rc = synk::ensure_max_smem((const void*)gemm_tc_persistent_kernel<1, false>, d->device, (int)smem); rc)
             return rc;
         const uint64_t tiles = ((M + BM - 1) / BM) * ((N + PBN - 1) / PBN);
         const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)d->num_sms);
-        gemm_tc_persistent_kernel<1><<<grid, PThreads, smem, d->stream>>>(a0, bw, (uint32_t)M, (uint32_t)N,
-                                                                            (uint32_t)K, e, lay);
+        gemm_tc_persistent_kernel<1, false><<<grid, PThreads, smem, d->stream>>>(a0, bw, bw, (uint32_t)M, (uint32_t)N,
+                                                                                   (uint32_t)K, e, lay);
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
         return SYNK_OK;
     }

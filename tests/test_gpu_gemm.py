@@ -244,9 +244,10 @@ def test_prep2_bf16_cast_and_transpose(rows, cols):
     np.testing.assert_array_equal(got_t, want.T.astype(np.uint16))
 
 
-def gemm_layout(R, a, b, layout, epi="store", bias=None, act=None, out_bf16=False):
+def gemm_layout(R, a, b, layout, epi="store", bias=None, act=None, out_bf16=False, want_t=None):
     """bf16 C = epi(a @ b.T) with A stored MN-major (as a.T, K x M) when
-    layout & 1 and B stored MN-major (as b.T, K x N) when layout & 2."""
+    layout & 1 and B stored MN-major (as b.T, K x N) when layout & 2.
+    want_t (not None): return (C, C^T or None), C^T requested when true."""
     M, K = a.shape
     N = b.shape[0]
     ahi, _, lda = prep(R, a.T if layout & 1 else a, False, 1)
@@ -260,14 +261,22 @@ def gemm_layout(R, a, b, layout, epi="store", bias=None, act=None, out_bf16=Fals
         da = R.upload(act.astype(np.float32))
         check(lib().synk_gemm_prep(R[0], F32, _vp(da), _u64(M), _u64(N), _u64(N), 0, 1, _vp(dact), None, _u64(M),
                                    _u64(N), _u64(N)), "prep act")
+    ct = R.alloc(M * N * es) if want_t else 0
     check(lib().synk_gemm_tc2(R[0], 0, _u64(M), _u64(N), _u64(K), _vp(ahi), None, _u64(lda), _vp(bhi), None, _u64(ldb),
-                              layout, EPI[epi], BF16 if out_bf16 else F32, _vp(c), _u64(N), None, _u64(0),
+                              layout, EPI[epi], BF16 if out_bf16 else F32, _vp(c), _u64(N), _vp(ct or None), _u64(M),
                               _vp(dbias or None), _vp(dact or None), _u64(N)), "gemm_tc2")
     check(R.sync(), "sync")
-    if out_bf16:
-        raw = R.download(c, (M, N), np.uint16).astype(np.uint32) << 16
-        return raw.view(np.float32)
-    return R.download(c, (M, N), np.float32)
+
+    def fetch(ptr, shape):
+        if out_bf16:
+            raw = R.download(ptr, shape, np.uint16).astype(np.uint32) << 16
+            return raw.view(np.float32)
+        return R.download(ptr, shape, np.float32)
+
+    out = fetch(c, (M, N))
+    if want_t is None:
+        return out
+    return out, (fetch(ct, (N, M)) if want_t else None)
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 200, 100), (129, 520, 72), (4096, 2048, 512),
@@ -305,6 +314,26 @@ def test_bf16_mn_major_fused_epilogues():
             act = bf16_round(np.tanh(rng.uniform(-1, 1, (M, N))))
             got = gemm_layout(R, a, b, layout, "tanh_grad", act=act, out_bf16=True)
             assert rel_err(got, z * (1 - act.astype(np.float64) ** 2)) <= 2.0 ** -7 * 4
+
+
+@pytest.mark.parametrize("M,N,K,with_t", [(8192, 4096, 100, False), (1000, 600, 100, True), (300, 260, 8, False),
+                                            (513, 4100, 128, True)])
+def test_bf16_short_k_tanh_grad_staged_activations(M, N, K, with_t):
+    """Short-K tanh-derivative products (C5's dX with K = 100): the CTA-pair
+    kernel TMA-stages each tile's activation block into shared memory while
+    the previous tile drains. Ragged M / N edges, K below one block, an
+    optional transposed output; checked against fp64 on bf16-exact inputs at
+    bf16 output resolution, and C^T bitwise equal to C."""
+    rng = np.random.default_rng(M + N + K)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)))
+    b = bf16_round(rng.uniform(-1, 1, (N, K)) * 0.1)
+    act = bf16_round(np.tanh(rng.uniform(-1, 1, (M, N))))
+    want = (a.astype(np.float64) @ b.astype(np.float64).T) * (1 - act.astype(np.float64) ** 2)
+    with Ranks(1) as R:
+        got, got_t = gemm_layout(R, a, b, 0, "tanh_grad", act=act, out_bf16=True, want_t=with_t)
+    assert rel_err(got, want) <= 2.0 ** -7 * 4
+    if with_t:
+        np.testing.assert_array_equal(got_t, got.T)
 
 
 def test_c5_full_size_bf16_gradient_vs_fp64(sk, oracle):
