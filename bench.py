@@ -804,7 +804,10 @@ def sync_sgd_section(sk, args, n_gpus, model, dry=False):
     back-to-back stretch (the sustained figure at the power cap)."""
     m = SGD_MODELS[model]
     runs = []
-    for n in gpu_counts(n_gpus):
+    # one rank per VISIBLE GPU: a job asking for more GPUs than the box shows
+    # (e.g. torchrun N=2 on a 1-GPU box) measures up to the visible count
+    n_vis = n_gpus if dry else min(n_gpus, max(1, sk.device_count()))
+    for n in gpu_counts(n_vis):
         devs = list(range(n))
         sus = 3.0 if n == 1 and model == "c5" else 0.0
         if dry:
@@ -814,6 +817,7 @@ def sync_sgd_section(sk, args, n_gpus, model, dry=False):
     scaling_summary(runs, model)
     top = runs[-1]
     out = {"config": m["label"] + ", batch %d per GPU (scaled)" % m["per_gpu"], "dtype": m["dtype"],
+           "gpus_visible_capped": None if n_vis == n_gpus else "%d of %d requested GPUs visible" % (n_vis, n_gpus),
            "flops_per_sample": flops_per_sample(m["dims"]), "runs": runs,
            "samples_per_s": top["samples_per_s"], "ms_per_step": top["ms_per_step"], "n_gpus": top["n_gpus"],
            "table1_note": "function = gradient-call compute (mean over ranks, device events); shuffle = staging of "
