@@ -95,7 +95,8 @@ def rel_err(got, want):
 # C1's five products (784-512-10, batch 256) plus ragged, single-tile,
 # split and unsplit shapes and a long K (where a plain TMEM chain drifts).
 SHAPES = [(256, 512, 784), (256, 10, 512), (513, 10, 256), (256, 512, 10), (785, 512, 256), (1, 1, 1),
-          (128, 128, 32), (300, 130, 1000), (64, 700, 4096), (256, 256, 8192)]
+          (128, 128, 32), (300, 130, 1000), (64, 700, 4096), (256, 256, 8192),
+          (2048, 2048, 256), (1700, 2100, 40)]  # the last two: >= 148 tiles of 128x128 -> 128-wide tiles, no split
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -128,7 +129,7 @@ def test_f32x3_all_positive_long_k_has_no_drift():
     assert abs(float(np.mean(rel))) <= 5e-7, float(np.mean(rel))
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 512, 784), (256, 10, 512), (100, 40, 64)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 784), (256, 10, 512), (100, 40, 64), (1664, 1800, 96)])
 @pytest.mark.parametrize("epi", ["bias", "bias_tanh", "tanh_grad"])
 def test_f32x3_epilogues_and_split_outputs(M, N, K, epi):
     rng = np.random.default_rng(M + N + K + len(epi))
