@@ -29,8 +29,9 @@ using synk::combine_op;
 
 constexpr int kMaxWorld = 64;
 constexpr int kBlock = 256;
-// The fused all-reduce + update: 256-thread CTAs, 4 per SM, one vector item
-// per thread per iteration (74 registers). Measured against 128-thread CTAs
+// The fused all-reduce + update: 256-thread CTAs, all resident at once
+// (synk::resident_grid), one vector item per thread per iteration (~80
+// registers). Measured against 128-thread CTAs
 // that co-reside with the persistent GEMM and two items in flight per thread
 // (122 registers): C5 1.053 vs 1.065-1.075 ms (serialised or overlapped), so
 // the occupancy of the streaming loop matters more than co-residency.
@@ -273,9 +274,9 @@ __device__ __forceinline__ void shadow_store(const Shadow& sh, int q, uint64_t g
 // U vector items per call (v[u], valid while v[u] < v_end): every load of
 // every item (W gradient replicas, params, aux) is issued before the first
 // use, so a thread has U x (W + 1 + naux) 16/32-byte loads in flight instead
-// of one dependent round trip per array -- the update runs beside the
-// persistent GEMMs with one 128-thread CTA per SM, where memory-level
-// parallelism per thread sets its bandwidth.
+// of one dependent round trip per array. The kernel instantiates U = 1: two
+// items per thread raised the registers to 122 and the resident CTAs per SM
+// fell, which cost more than the extra loads in flight bought (kStepBlock).
 template <class T, int W, int BYTES, bool SH, int U, int RULE>
 __device__ __forceinline__ void step_vectors(const Ptrs& params, const Ptrs& grads, const Ptrs& aux0, const Ptrs& aux1,
                                              int rank, int grad_op, int fop, double inv_w, const synk::RuleParams& rp,
