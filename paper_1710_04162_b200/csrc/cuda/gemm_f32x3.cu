@@ -2,9 +2,9 @@
 // mlp.cpp:31-73 products), sm_100a only:
 //   C[M x N] = epilogue( A[M x K] . B[N x K]^T )
 // A and B are K-major fp32 matrices handed over as tf32 hi + lo parts
-// (hi = rna_tf32(x), lo = rna_tf32(x - hi); tf32_split_kernel below, or the
+// (hi = rna_tf32(x), lo = rna_tf32(x - hi); tf32_stage_kernel below, or the
 // epilogue of the producing GEMM). Per 32-element K block the MMA warp issues
-// hi.lo + lo.hi + hi.hi (tcgen05.mma kind::tf32, 12 MMAs of 128x128x8) into a
+// hi.lo + lo.hi + hi.hi (tcgen05.mma kind::tf32, 12 MMAs of 128xBNx8) into a
 // FRESH TMEM accumulator; the four epilogue warps then drain that block sum
 // into fp32 registers with round-to-nearest adds while the MMA warp fills the
 // other of two TMEM buffers. The tensor-core accumulator therefore never
@@ -13,16 +13,21 @@
 // stays at the single-block level (~-1e-7) instead of growing with K, and the
 // small correction products are accumulated before the large hi.hi ones.
 //
-// Split K: when the output has too few 128x128 tiles to fill the GPU, the
-// S <= 8 CTAs of a tile (one per K range, a thread-block cluster along z)
-// park their fp32 partials in shared memory and CTA z folds rows
-// [z*R, (z+1)*R) across the S partials in rank order with an f64 accumulator
-// (distributed shared memory, no HBM planes, no fold launch). S depends on
-// the shape only, so results do not depend on the device.
+// Tiles are 128 x BN: BN = 64 when the 128x128 tiling has fewer tiles than
+// SMs (the C1 products: twice the CTAs, shorter epilogues, two CTAs per SM),
+// else 128. Split K: when the tiles cannot fill the GPU, the S <= 8 CTAs of a
+// tile (one per K range, a thread-block cluster along z, sized so every
+// cluster fits in one wave) park their fp32 partials in shared memory and CTA
+// z folds rows [z*R, (z+1)*R) across the S partials in rank order with an f64
+// accumulator (distributed shared memory, no HBM planes, no fold launch). S
+// depends on the shape and CTA footprint only, never on the device.
 //
 // Epilogue outputs (any subset): C (fp32, row-major), the tf32 hi/lo split of
 // the result row-major and/or transposed -- so a layer's activation or delta
-// is emitted directly in the operand form the next products read.
+// is emitted directly in the operand form the next products read. The
+// epilogue kinds the MLP issues are compiled as specialisations (a CTA runs
+// its epilogue once, from a cold instruction cache), and the tanh' activation
+// tile is TMA-staged into shared memory during the main loop.
 //
 // Warp roles (192 threads): 0 TMA producer (one lane), 1 MMA issuer (one
 // lane), 2..5 accumulators/epilogue (warp w reads TMEM lane quadrant w % 4;
