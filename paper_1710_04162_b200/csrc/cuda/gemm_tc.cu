@@ -21,8 +21,12 @@
 // same TMEM accumulator (3 passes over K). Products are then exact, but the
 // tcgen05 fp32 accumulator itself rounds with a bias of ~-6.7e-9 per
 // accumulated product (profiles/r01_tcgen05_tf32_accumulation.txt), so long K
-// chains drift past the 1e-5 fp32 bar; the f32 example function therefore
-// stays on FFMA and this kernel's production use is bf16 (kind 0).
+// chains drift past the 1e-5 fp32 bar. This kind stays as the C-ABI's plain
+// 3xTF32 GEMM; the f32 example function runs on gemm_f32x3.cu, which restarts
+// the TMEM accumulator every K block and sums the blocks in fp32 registers.
+// Production use of this file is bf16 (kind 0): this non-persistent kernel
+// for the narrow (N <= 128) products, the persistent CTA-pair kernel below
+// for the wide ones.
 //
 // Occupancy: 3 stages x 32 KB + barriers ~ 97 KB smem and 128 TMEM columns per
 // CTA, so two CTAs share an SM and one CTA's epilogue overlaps the other's
