@@ -2,6 +2,8 @@
 
 #include "transfer.hpp"
 
+#include <algorithm>
+
 #include <cstring>
 #include <vector>
 
@@ -38,8 +40,18 @@ void validate_view(const SelView& sel, std::size_t n) {
         validate_selection(IndexSelection(sel.range), n);
         return;
     }
-    std::uint64_t hi = 0;
-    for (std::size_t i = 0; i < sel.count; ++i) hi = sel.list[i] > hi ? sel.list[i] : hi;
+    // four independent maxima: no loop-carried dependency through one cmov
+    // (the per-step host bounds check of C5's 8192-entry index list)
+    std::uint64_t h0 = 0, h1 = 0, h2 = 0, h3 = 0;
+    std::size_t i = 0;
+    for (; i + 4 <= sel.count; i += 4) {
+        h0 = sel.list[i] > h0 ? sel.list[i] : h0;
+        h1 = sel.list[i + 1] > h1 ? sel.list[i + 1] : h1;
+        h2 = sel.list[i + 2] > h2 ? sel.list[i + 2] : h2;
+        h3 = sel.list[i + 3] > h3 ? sel.list[i + 3] : h3;
+    }
+    for (; i < sel.count; ++i) h0 = sel.list[i] > h0 ? sel.list[i] : h0;
+    const std::uint64_t hi = std::max(std::max(h0, h1), std::max(h2, h3));
     if (sel.count == 0 || hi < n) return;
     for (std::size_t i = 0; i < sel.count; ++i)
         if (sel.list[i] >= n)
