@@ -32,6 +32,9 @@ public:
                            std::vector<std::size_t> shape, DType dtype);
     static DevBuffer zeros(const std::shared_ptr<detail::RankDevice>& owner,
                            std::vector<std::size_t> shape, DType dtype);
+    // `bytes` of device-accessible memory this buffer does not own (e.g. the
+    // rank's mapped pinned staging); views of it come from reinterpret().
+    static DevBuffer wrap_external(const std::shared_ptr<detail::RankDevice>& owner, void* ptr, std::size_t bytes);
 
     const std::vector<std::size_t>& shape() const noexcept { return shape_; }
     std::size_t rank() const noexcept { return shape_.size(); }

@@ -103,6 +103,13 @@ struct KernelContext {
         int ready_slot = -1;
     };
     const std::vector<IndexedInput>* indexed = nullptr;
+    // Single-contributor calls (one rank, one slice): the rank's mapped pinned
+    // staging, offered for small outputs. device_alloc places buffers of at
+    // most 4 KiB there, so the phase hands them to the host without a copy
+    // kernel (the output staging of function.cpp:515-527 without a launch).
+    // Empty when not offered.
+    DevBuffer host_staging;
+    mutable std::size_t host_staging_used = 0;
 };
 
 struct KernelResult {

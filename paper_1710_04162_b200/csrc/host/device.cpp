@@ -81,7 +81,7 @@ void* rank_scratch(const std::shared_ptr<RankDevice>& rd, std::size_t bytes) {
 }
 
 DevStorage::~DevStorage() {
-    if (ptr && owner) owner->release_block(ptr, bytes);
+    if (ptr && owner && !external) owner->release_block(ptr, bytes);
 }
 
 int synk_dtype(DType dt) { return dt == DType::Float32 ? SYNK_F32 : SYNK_F64; }
@@ -154,6 +154,19 @@ DevBuffer DevBuffer::alloc(const std::shared_ptr<detail::RankDevice>& owner, std
     st->owner = owner;
     st->bytes = b.byte_size();
     if (st->bytes) st->ptr = owner->take_block(st->bytes);
+    b.store_ = std::move(st);
+    return b;
+}
+
+DevBuffer DevBuffer::wrap_external(const std::shared_ptr<detail::RankDevice>& owner, void* ptr, std::size_t bytes) {
+    DevBuffer b;
+    b.shape_ = {bytes};
+    b.dtype_ = DType::Float64;  // bookkeeping only: views reinterpret it
+    auto st = std::make_shared<detail::DevStorage>();
+    st->owner = owner;
+    st->bytes = bytes;
+    st->ptr = ptr;
+    st->external = true;
     b.store_ = std::move(st);
     return b;
 }

@@ -88,6 +88,7 @@ struct DevStorage {
     void* ptr = nullptr;
     std::size_t bytes = 0;
     std::shared_ptr<RankDevice> owner;
+    bool external = false;  // not owned (e.g. the rank's mapped pinned staging): never released
     ~DevStorage();
 };
 

@@ -122,7 +122,10 @@ std::pair<DevBuffer, DevBuffer> device_loss_grad(const std::shared_ptr<detail::R
     detail::check(synk_mlp_workspace_bytes_ex(detail::synk_dtype(dt), mode, c.dims.data(), L, c.n, &ws_bytes),
                   "mlp workspace");
     void* ws = detail::rank_scratch(rd, ws_bytes);
-    DevBuffer loss = DevBuffer::alloc(rd, {}, DType::Float64);
+    // the loss may land straight in the rank's pinned staging (single
+    // contributor: KernelContext::host_staging), read by the host after the phase
+    DevBuffer loss = ctx && ctx->rank_device == rd ? ctx->device_alloc({}, DType::Float64)
+                                                   : DevBuffer::alloc(rd, {}, DType::Float64);
     DevBuffer grad = DevBuffer::alloc(rd, {params.size()}, dt);
     synk_mlp_opts opts{};
     opts.signal_base = ctx && ctx->grad_segments ? ctx->grad_signal_base : -1;
