@@ -163,6 +163,16 @@ int synk_cast(synk_dev* dev, int dst_dtype, void* dst, int src_dtype, const void
  * the next synk_sync(). */
 int synk_gather_rows(synk_dev* dev, const void* src, uint64_t src_rows, uint64_t row_bytes,
                      const uint64_t* idx, uint64_t n_idx, void* dst);
+/* The same for a short list in HOST memory (pageable or pinned), read by the
+ * calling thread: n_idx <= SYNK_GATHER_INLINE_MAX and src_rows <= 2^32. The
+ * indices travel inside the kernel launch (u32 kernel parameters), so the
+ * kernel's first row loads do not wait on PCIe index reads -- the per-call
+ * floor of one small batch (excerpt_rows, tensor.cpp:399-409, per call).
+ * Bit-exact with synk_gather_rows; an out-of-range index reads row 0 and
+ * raises SYNK_EBOUNDS at the next synk_sync(). */
+#define SYNK_GATHER_INLINE_MAX 4096
+int synk_gather_rows_inline(synk_dev* dev, const void* src, uint64_t src_rows, uint64_t row_bytes,
+                            const uint64_t* host_idx, uint64_t n_idx, void* dst);
 
 /* ---- aggregation --------------------------------------------------------------- */
 /* acc = op(acc, other), op in {sum,max,min,prod}, in T (combine_inplace,

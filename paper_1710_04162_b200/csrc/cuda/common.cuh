@@ -28,6 +28,10 @@ struct synk_dev {
     void* graphs = nullptr;          // CUDA-graph cache of the MLP loss/grad launch sequence (mlp.cu)
     void* nccl = nullptr;            // ncclComm_t of the optional NCCL backend (nccl_backend.cu)
     int marks_used = 0;
+    // The last launch on `stream` released its dependents at entry
+    // (griddepcontrol.launch_dependents): the next small follow-up kernel may
+    // launch programmatically (PDL) and overlap its launch with that kernel.
+    bool pdl_armed = false;
 };
 
 namespace synk {
@@ -44,6 +48,32 @@ int ensure_max_smem(const void* kernel, int device, int bytes);
 int prefer_shared_carveout(const void* kernel, int device);
 // Grid that keeps every CTA of a grid-stride kernel resident at once.
 unsigned resident_grid(const void* kernel, int device, int block, uint64_t work_items);
+
+// Launch a small follow-up kernel on d->stream, programmatically dependent
+// (PDL) on the previous launch when that one armed it (synk_dev::pdl_armed):
+// its CTAs are scheduled while the previous kernel still runs and block in
+// griddepcontrol.wait -- which every kernel launched here executes before its
+// first global access -- until that kernel completed and its writes are
+// visible. Un-armed, it is an ordinary stream-ordered launch.
+template <class... KArgs, class... Args>
+cudaError_t launch_follow_up(synk_dev* d, void (*kernel)(KArgs...), unsigned grid, unsigned block, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = d->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = d->pdl_armed ? 1 : 0;
+    d->pdl_armed = false;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+__device__ __forceinline__ void wait_prerequisite_grid() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void release_dependent_grid() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Releases the rank's graph cache (mlp.cu); called by synk_close.
 void release_graphs(synk_dev* d);

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kBlock) scale_kernel(T* __restrict__ a, uint64
 
 template <class T>
 __global__ void __launch_bounds__(kBlock) fill_kernel(T* __restrict__ a, uint64_t n, T v) {
+    synk::wait_prerequisite_grid();  // no-op unless launched as a follow-up
     uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
     for (uint64_t i = tid; i < n; i += (uint64_t)gridDim.x * kBlock) a[i] = v;
 }
@@ -453,6 +454,7 @@ namespace {
 // Small copies by the SMs (one CTA): into mapped pinned host memory the
 // stores are posted PCIe writes, cheaper than a copy-engine round trip.
 __global__ void copy_small_kernel(char* __restrict__ dst, const char* __restrict__ src, uint64_t bytes) {
+    synk::wait_prerequisite_grid();  // launched as a follow-up (synk::launch_follow_up)
     const bool v16 = ((uintptr_t)dst | (uintptr_t)src | bytes) % 16 == 0;
     if (v16) {
         for (uint64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
@@ -470,7 +472,7 @@ int synk_copy_small(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
     SYNK_REQUIRE(bytes <= (1u << 20), SYNK_EARG, "synk_copy_small: at most 1 MiB");
     synk::DeviceGuard g(d->device);
     if (int rc = synk::prefer_shared_carveout((const void*)copy_small_kernel, d->device); rc) return rc;
-    copy_small_kernel<<<1, 256, 0, d->stream>>>((char*)dst, (const char*)src, bytes);
+    SYNK_CU(synk::launch_follow_up(d, copy_small_kernel, 1, 256, (char*)dst, (const char*)src, bytes));
     SYNK_LAUNCHED("copy_small_kernel");
     return SYNK_OK;
 }
@@ -480,8 +482,14 @@ int synk_fill(synk_dev* d, int dtype, void* dst, double value, uint64_t n) {
     if (n == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     unsigned grid = synk::grid_for(d, n, kBlock);
-    if (dtype == SYNK_F32) fill_kernel<float><<<grid, kBlock, 0, d->stream>>>((float*)dst, n, (float)value);
-    else fill_kernel<double><<<grid, kBlock, 0, d->stream>>>((double*)dst, n, value);
+    if (grid == 1) {  // small fill (a kernel's scalar result): a follow-up launch
+        if (dtype == SYNK_F32) SYNK_CU(synk::launch_follow_up(d, fill_kernel<float>, 1, kBlock, (float*)dst, n, (float)value));
+        else SYNK_CU(synk::launch_follow_up(d, fill_kernel<double>, 1, kBlock, (double*)dst, n, value));
+    } else {
+        d->pdl_armed = false;
+        if (dtype == SYNK_F32) fill_kernel<float><<<grid, kBlock, 0, d->stream>>>((float*)dst, n, (float)value);
+        else fill_kernel<double><<<grid, kBlock, 0, d->stream>>>((double*)dst, n, value);
+    }
     SYNK_LAUNCHED("fill_kernel");
     return SYNK_OK;
 }

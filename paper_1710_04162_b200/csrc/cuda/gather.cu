@@ -152,6 +152,72 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
     }
 }
 
+// Short host-side lists (<= SYNK_GATHER_INLINE_MAX indices below 2^32) travel
+// inside the launch: the u32 indices are a kernel parameter (constant bank,
+// fetched with the launch), so no warp waits on a dependent PCIe read of a
+// pinned list before its first row load -- the latency floor of one small
+// batch per call (bench single_batch_call). The host validated the list while
+// narrowing it. Warp w streams rows 4w..4w+3; dependents are released at entry.
+}  // namespace
+namespace synk {
+uint32_t narrow_indices(const uint64_t* in, uint64_t n, uint64_t limit, uint32_t* out);  // index_narrow.cpp
+}  // namespace synk
+namespace {
+
+struct InlineIdx {
+    uint32_t idx[SYNK_GATHER_INLINE_MAX];
+};
+static_assert(sizeof(InlineIdx) + 64 <= 32764, "kernel parameter limit");
+
+template <int BYTES, int kUnroll>
+__global__ void __launch_bounds__(kBlock) gather_rows_inline_kernel(const typename Vec<BYTES>::T* __restrict__ src,
+                                                                    uint64_t row_vecs,
+                                                                    const __grid_constant__ InlineIdx p,
+                                                                    uint32_t n_idx,
+                                                                    typename Vec<BYTES>::T* __restrict__ dst) {
+    using V = typename Vec<BYTES>::T;
+    synk::release_dependent_grid();
+    const int lane = threadIdx.x & 31;
+    const uint32_t r0 = ((blockIdx.x * kBlock + threadIdx.x) >> 5) * 4;
+    if (r0 >= n_idx) return;
+    uint64_t row[4];
+    int exists[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        exists[k] = r0 + k < n_idx;
+        row[k] = exists[k] ? p.idx[r0 + k] : 0;
+    }
+    for (uint64_t v0 = lane; v0 < row_vecs; v0 += 32 * kUnroll) {
+        V buf[4][kUnroll];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint64_t v = v0 + (uint64_t)u * 32;
+                if (exists[k] && v < row_vecs) buf[k][u] = Vec<BYTES>::load(src + row[k] * row_vecs + v);
+            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint64_t v = v0 + (uint64_t)u * 32;
+                if (exists[k] && v < row_vecs) store_vec(dst + ((uint64_t)r0 + k) * row_vecs + v, buf[k][u], 0);
+            }
+    }
+}
+
+template <int BYTES>
+int launch_inline(synk_dev* d, const void* src, uint64_t row_bytes, const InlineIdx& p, uint32_t n_idx, void* dst) {
+    using V = typename Vec<BYTES>::T;
+    const unsigned blocks = (unsigned)(((uint64_t)(n_idx + 3) / 4 * 32 + kBlock - 1) / kBlock);
+    constexpr int U = BYTES == 32 ? 1 : 2;
+    gather_rows_inline_kernel<BYTES, U><<<blocks, kBlock, 0, d->stream>>>((const V*)src, row_bytes / BYTES, p, n_idx,
+                                                                           (V*)dst);
+    SYNK_LAUNCHED("gather_rows_inline_kernel");
+    d->pdl_armed = true;
+    return SYNK_OK;
+}
+
 template <int BYTES, int R, int U, int MB>
 void launch_variant(synk_dev* d, unsigned blocks, const void* src, uint64_t src_rows, uint64_t row_bytes,
                     const uint64_t* idx, uint64_t n_idx, uint32_t chunk, void* dst) {
@@ -491,6 +557,27 @@ int launch_bulk(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_by
 }
 
 }  // namespace
+
+extern "C" int synk_gather_rows_inline(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
+                                       const uint64_t* host_idx, uint64_t n_idx, void* dst) {
+    if (n_idx == 0 || row_bytes == 0) return SYNK_OK;
+    SYNK_REQUIRE(n_idx <= SYNK_GATHER_INLINE_MAX, SYNK_EARG, "synk_gather_rows_inline: list longer than the inline maximum");
+    SYNK_REQUIRE(src_rows <= (1ull << 32), SYNK_EARG, "synk_gather_rows_inline: source rows past 2^32");
+    InlineIdx p;
+    // Narrow + bounds check in one pass (index_narrow.cpp); an out-of-range
+    // index reads row 0 (defined data) and raises the rank's sticky flag, so
+    // the call fails with SYNK_EBOUNDS at the next synk_sync() exactly like
+    // the device check.
+    if (synk::narrow_indices(host_idx, n_idx, src_rows, p.idx)) d->err_host[0] = 1;
+    synk::DeviceGuard g(d->device);
+    const uint64_t a = row_bytes | (uint64_t)(uintptr_t)src | (uint64_t)(uintptr_t)dst;
+    const uint32_t n = (uint32_t)n_idx;
+    if ((a & 31) == 0) return launch_inline<32>(d, src, row_bytes, p, n, dst);
+    if ((a & 15) == 0) return launch_inline<16>(d, src, row_bytes, p, n, dst);
+    if ((a & 7) == 0) return launch_inline<8>(d, src, row_bytes, p, n, dst);
+    if ((a & 3) == 0) return launch_inline<4>(d, src, row_bytes, p, n, dst);
+    return launch_inline<1>(d, src, row_bytes, p, n, dst);
+}
 
 extern "C" int synk_gather_rows(synk_dev* d, const void* src, uint64_t src_rows,
                                 uint64_t row_bytes, const uint64_t* idx, uint64_t n_idx,

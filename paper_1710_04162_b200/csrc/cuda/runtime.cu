@@ -216,6 +216,7 @@ int synk_bind(const synk_dev* d) {
 
 int synk_sync(synk_dev* d) {
     DeviceGuard g(d->device);
+    d->pdl_armed = false;
     SYNK_CU(cudaStreamSynchronize(d->stream));
     if (d->err_host[0] != 0) {
         d->err_host[0] = 0;

@@ -101,22 +101,6 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
     if (part.stop > sel.count) throw BoundsError("excerpt_rows(): part extends past the index list");
     DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
     if (part.count() == 0 || row_bytes == 0) return out;
-    const std::pair<const std::uint64_t*, std::size_t> key{sel.list + part.start, part.count()};
-    DevBuffer idx;
-    const std::uint64_t* idx_ptr = nullptr;
-    if (const std::uint64_t* dv = device_view(key.first)) {
-        idx_ptr = dv;  // pinned list: the gather kernel reads it in place over PCIe
-    } else {
-        if (uploads)
-            for (auto& [k, buf] : uploads->done)
-                if (k == key) idx = buf;
-        if (!idx.has_storage()) {
-            idx = upload_indices(rd, key.first, key.second);
-            if (uploads) uploads->done.emplace_back(key, idx);
-        }
-        idx_ptr = static_cast<const std::uint64_t*>(idx.data());
-    }
-
     const void* base = nullptr;
     DevBuffer staged;  // keeps a device copy alive when the host source is pageable
     if (have_mirror) {
@@ -144,6 +128,29 @@ DevBuffer excerpt_to_device(const std::shared_ptr<RankDevice>& rd, const NdBuffe
         check(synk_copy(rd->h, staged.data(), src.bytes(), src.byte_size()), "excerpt: stage pageable source");
         base = staged.data();
     }
+    const std::pair<const std::uint64_t*, std::size_t> key{sel.list + part.start, part.count()};
+    if (key.second <= SYNK_GATHER_INLINE_MAX && n_src <= (std::size_t(1) << 32)) {
+        // one short batch: the list rides in the launch (no PCIe index reads,
+        // no upload), pageable or pinned alike
+        check(synk_gather_rows_inline(rd->h, base, n_src, row_bytes, key.first, key.second, out.data()),
+              "gather_rows (inline list)");
+        return out;
+    }
+    DevBuffer idx;
+    const std::uint64_t* idx_ptr = nullptr;
+    if (const std::uint64_t* dv = device_view(key.first)) {
+        idx_ptr = dv;  // pinned list: the gather kernel reads it in place over PCIe
+    } else {
+        if (uploads)
+            for (auto& [k, buf] : uploads->done)
+                if (k == key) idx = buf;
+        if (!idx.has_storage()) {
+            idx = upload_indices(rd, key.first, key.second);
+            if (uploads) uploads->done.emplace_back(key, idx);
+        }
+        idx_ptr = static_cast<const std::uint64_t*>(idx.data());
+    }
+
     check(synk_gather_rows(rd->h, base, n_src, row_bytes, idx_ptr, part.count(), out.data()), "gather_rows");
     return out;
 }
@@ -156,6 +163,12 @@ DevBuffer select_device_rows(const std::shared_ptr<RankDevice>& rd, const DevBuf
     DevBuffer out = DevBuffer::alloc(rd, std::move(shape), src.dtype());
     const std::size_t row_bytes = src.row_size() * dtype_size(src.dtype());
     if (list.empty() || row_bytes == 0) return out;
+    const auto* l = reinterpret_cast<const std::uint64_t*>(list.data());
+    if (list.size() <= SYNK_GATHER_INLINE_MAX && src.rows() <= (std::size_t(1) << 32)) {
+        check(synk_gather_rows_inline(rd->h, src.data(), src.rows(), row_bytes, l, list.size(), out.data()),
+              "gather_rows (replica, inline list)");
+        return out;
+    }
     DevBuffer idx = upload_indices(rd, reinterpret_cast<const std::uint64_t*>(list.data()), list.size());
     check(synk_gather_rows(rd->h, src.data(), src.rows(), row_bytes, static_cast<const std::uint64_t*>(idx.data()),
                            list.size(), out.data()),

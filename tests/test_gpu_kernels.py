@@ -157,6 +157,84 @@ def test_gather_index_list_in_pinned_host_memory(oracle):
             assert R.download(d_out, (n_idx, 256), np.float32).tobytes() == oracle.gather_rows(src, idx).tobytes()
 
 
+def test_gather_inline_list_bit_exact(oracle):
+    """synk_gather_rows_inline: a host list (pageable numpy memory) of at most
+    SYNK_GATHER_INLINE_MAX indices rides in the launch as u32 kernel
+    parameters. Every vector width (1/4/8/16/32-byte lanes by row size and
+    alignment), ragged counts, and the golden vectors."""
+    rng = np.random.default_rng(6)
+    with Ranks(1) as R:
+        for dtype, shape in ((np.float32, (10000, 256)), (np.float32, (513, 37)), (np.float64, (300, 8)),
+                             (np.float32, (64, 10)), (np.float64, (5, 1)), (np.uint8, (777, 3)),
+                             (np.float32, (300, 1028)), (np.float64, (257, 1024))):
+            src = (rng.uniform(-1, 1, shape) * 100).astype(dtype)
+            d_src = R.upload(src)
+            for n_idx in (1, 3, 4, 5, 31, 33, 1000, 4095, 4096):
+                idx = rng.integers(0, shape[0], n_idx).astype(np.uint64)
+                d_out = R.alloc(n_idx * src[0].nbytes)
+                check(lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(shape[0]), _u64(src[0].nbytes),
+                                                    idx.ctypes.data_as(_vp), _u64(n_idx), _vp(d_out)), "gather inline")
+                check(R.sync(), "sync")
+                got = R.download(d_out, (n_idx,) + shape[1:], dtype)
+                assert got.tobytes() == oracle.gather_rows(src, idx).tobytes(), (shape, n_idx)
+        g = golden("gather.npz")
+        for tag in ("f32", "f64"):
+            src, idx = g[tag + "_src"], np.ascontiguousarray(g[tag + "_idx"].astype(np.uint64))
+            d_src, d_out = R.upload(src), R.alloc(len(idx) * src[0].nbytes)
+            check(lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(src.shape[0]), _u64(src[0].nbytes),
+                                                idx.ctypes.data_as(_vp), _u64(len(idx)), _vp(d_out)), "gather inline")
+            assert R.download(d_out, (len(idx),) + src.shape[1:], src.dtype).tobytes() == g[tag + "_w3_list"].tobytes()
+
+
+def test_gather_inline_list_bounds_and_limits():
+    """Out-of-range index: row 0 is read, SYNK_EBOUNDS at the next sync, then
+    cleared (the device check's contract). Lists past the inline maximum or
+    sources past 2^32 rows are refused (SYNK_EARG), nothing launched."""
+    with Ranks(1) as R:
+        src = np.arange(8, dtype=np.float64).reshape(4, 2)
+        d_src, d_out = R.upload(src), R.alloc(32)
+        bad = np.array([1, 4], np.uint64)
+        check(lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(4), _u64(16), bad.ctypes.data_as(_vp), _u64(2),
+                                            _vp(d_out)), "g")
+        assert R.sync() == -1  # SYNK_EBOUNDS
+        assert R.sync() == 0
+        assert R.download(d_out, (2, 2), np.float64).tolist() == [[2.0, 3.0], [0.0, 1.0]]
+        long = np.zeros(4097, np.uint64)
+        assert lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(4), _u64(16), long.ctypes.data_as(_vp),
+                                             _u64(4097), _vp(d_out)) != 0
+        assert lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(1 << 33), _u64(16), bad.ctypes.data_as(_vp),
+                                             _u64(2), _vp(d_out)) != 0
+        assert lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(4), _u64(16), bad.ctypes.data_as(_vp), _u64(0),
+                                             _vp(d_out)) == 0
+        check(R.sync(), "sync")
+
+
+def test_follow_up_fill_and_copy_after_inline_gather():
+    """The inline gather releases its dependents at entry; a small fill or
+    copy_small right behind it launches programmatically (PDL) and must still
+    see the gather's rows: copy_small reads the gathered block, fill writes
+    over part of it (its store lands after every gather store)."""
+    rng = np.random.default_rng(7)
+    src = rng.uniform(-1, 1, (20000, 256)).astype(np.float32)
+    with Ranks(1) as R:
+        d_src = R.upload(src)
+        for it in range(20):
+            idx = rng.integers(0, 20000, 4096).astype(np.uint64)
+            d_out, d_cp = R.alloc(4096 * 1024), R.alloc(4096 * 1024)
+            check(lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(20000), _u64(1024), idx.ctypes.data_as(_vp),
+                                                _u64(4096), _vp(d_out)), "g")
+            check(lib().synk_copy_small(R[0], _vp(d_cp), _vp(d_out + 4095 * 1024), _u64(1024)), "copy_small")
+            check(lib().synk_gather_rows_inline(R[0], _vp(d_src), _u64(20000), _u64(1024), idx.ctypes.data_as(_vp),
+                                                _u64(4096), _vp(d_out)), "g")
+            check(lib().synk_fill(R[0], F32, _vp(d_out + 4095 * 1024), ctypes.c_double(it), _u64(256)), "fill")
+            check(R.sync(), "sync")
+            want = src[idx]
+            assert R.download(d_cp, (1, 256), np.float32).tobytes() == want[4095:].tobytes()
+            got = R.download(d_out, (4096, 256), np.float32)
+            assert got[:4095].tobytes() == want[:4095].tobytes()
+            assert (got[4095] == it).all()
+
+
 def test_gather_out_of_range_raises_bounds():
     with Ranks(1) as R:
         src = np.zeros((4, 2))

@@ -14,7 +14,7 @@ sys.path.insert(0, ".")
 import paper_1710_04162_b200 as sk  # noqa: E402
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
-n_step = 4096 * 64
+n_step = int(sys.argv[2]) if len(sys.argv) > 2 else 4096 * 64
 rng = np.random.default_rng(0)
 torch.cuda.init()
 with sk.Pool(workers=1) as pool:
@@ -34,6 +34,26 @@ with sk.Pool(workers=1) as pool:
         f.call([arr], indexes=idx[s])
     dt = (time.perf_counter() - t0) / 30
     print("untraced: %.1f us/call = %.0f GB/s" % (1e6 * dt, n_step * 2056 / dt / 1e9))
+    # floors on this box: one torch kernel + stream sync, and sync alone
+    x = torch.zeros(1, device="cuda")
+    for _ in range(100):
+        x.add_(1)
+        torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(1000):
+        x.add_(1)
+        torch.cuda.synchronize()
+    print("torch 1 kernel + sync: %.1f us" % (1e3 * (time.perf_counter() - t0)))
+    t0 = time.perf_counter()
+    for _ in range(1000):
+        x.add_(1)
+        x.add_(1)
+        torch.cuda.synchronize()
+    print("torch 2 kernels + sync: %.1f us" % (1e3 * (time.perf_counter() - t0)))
+    t0 = time.perf_counter()
+    for _ in range(1000):
+        torch.cuda.synchronize()
+    print("sync alone: %.1f us" % (1e3 * (time.perf_counter() - t0)))
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for s in range(35, 40):
             f.call([arr], indexes=idx[s])
