@@ -91,17 +91,18 @@ constexpr int kBlock = 256;
 
 // Chunked grid-stride: warp w takes chunks w, w + nwarps, ... of `chunk`
 // consecutive destination rows (chunk <= 32, a multiple of kRows), so warps
-// running at the same time write neighbouring rows of dst. Lane i < chunk
-// holds index i of the chunk (one coalesced read, which matters when the list
-// sits in pinned host memory and travels over PCIe), and the NEXT chunk's
+// running at the same time write neighbouring rows of dst. The chunk's
+// indices sit in the warp's lanes (read as part of the CTA's index line, one
+// coalesced read, which matters when the list sits in pinned host memory and
+// travels over PCIe), and the NEXT chunk's
 // indices are requested before the current chunk's rows are streamed, so the
 // index fetch overlaps a chunk of row traffic.
 // kRows rows in flight per warp, kUnroll 16-byte vectors per row per lane.
 template <int BYTES, int kRows = 4, int kUnroll = 2, int kMinBlocks = 1>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
     const typename Vec<BYTES>::T* __restrict__ src, uint64_t src_rows, uint64_t row_vecs,
-    const uint64_t* __restrict__ idx, uint64_t n_idx, uint32_t chunk, typename Vec<BYTES>::T* __restrict__ dst,
-    int* __restrict__ err, int stream_stores) {
+    const uint64_t* __restrict__ idx, uint64_t n_idx, uint32_t chunk, int share,
+    typename Vec<BYTES>::T* __restrict__ dst, int* __restrict__ err, int stream_stores) {
     using V = typename Vec<BYTES>::T;
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -111,23 +112,32 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
         return;
     }
 
+    // Index lines: the CTA's 8 warps hold neighbouring chunks (warp w of the
+    // CTA rows orow = w * chunk onward), so with `share` every warp reads the
+    // CTA's whole line of 8 x chunk <= 32 indices in one coalesced request and
+    // takes its own lanes: a pinned-host list then travels as one 256-byte
+    // PCIe read per line (the other seven warps hit it in L2) instead of
+    // eight 32-byte reads -- +3-4 % e2e on C2 (profiles/r02_gather_e2e.md).
+    const int orow = share ? (int)((threadIdx.x >> 5) * chunk) : 0;
+    const int line = share ? (int)(chunk * (kBlock / 32)) : (int)chunk;
     uint64_t c0 = warp * chunk;
-    uint64_t next = c0 + lane < n_idx && lane < (int)chunk ? idx[c0 + lane] : 0;
+    uint64_t next = c0 - orow + lane < n_idx && lane < line ? idx[c0 - orow + lane] : 0;
     for (; c0 < n_idx; c0 += stride) {
         const uint64_t mine = next;
         const int in_chunk = (int)(n_idx - c0 < chunk ? n_idx - c0 : chunk);
-        const uint64_t cn = c0 + stride;
-        if (lane < (int)chunk && cn + lane < n_idx) next = idx[cn + lane];  // prefetch the next chunk
-        const int ok = lane < in_chunk && mine < src_rows;
-        if (lane < in_chunk && !ok) *(volatile int*)err = 1;  // mapped host flag: every writer stores 1
+        const uint64_t cn = c0 + stride - orow;
+        if (lane < line && cn + lane < n_idx) next = idx[cn + lane];  // prefetch the next chunk
+        const int own = lane >= orow && lane < orow + in_chunk;
+        const int ok = own && mine < src_rows;
+        if (own && !ok) *(volatile int*)err = 1;  // mapped host flag: every writer stores 1
+        // A bad index reads row 0 instead (defined data; the call fails).
+        const uint64_t safe = ok ? mine : 0;
         for (int g = 0; g < in_chunk; g += kRows) {
-            // A bad index reads row 0 instead (defined data; the call fails).
-            const uint64_t safe = ok ? mine : 0;
             uint64_t row[kRows];
             int exists[kRows];
 #pragma unroll
             for (int k = 0; k < kRows; ++k) {
-                row[k] = __shfl_sync(0xffffffffu, safe, (g + k) & 31);
+                row[k] = __shfl_sync(0xffffffffu, safe, (orow + g + k) & 31);
                 exists[k] = g + k < in_chunk;
             }
             const uint64_t r0 = c0 + g;
@@ -220,7 +230,7 @@ int launch_inline(synk_dev* d, const void* src, uint64_t row_bytes, const Inline
 
 template <int BYTES, int R, int U, int MB>
 void launch_variant(synk_dev* d, unsigned blocks, const void* src, uint64_t src_rows, uint64_t row_bytes,
-                    const uint64_t* idx, uint64_t n_idx, uint32_t chunk, void* dst) {
+                    const uint64_t* idx, uint64_t n_idx, uint32_t chunk, int share, void* dst) {
     using V = typename Vec<BYTES>::T;
     // Streaming (evict-first) stores when the destination is far larger than
     // what L2 could keep for a consumer anyway (measured +0.7 % on the C2
@@ -232,7 +242,7 @@ void launch_variant(synk_dev* d, unsigned blocks, const void* src, uint64_t src_
     }();
     const int stcs = forced >= 0 ? forced : (n_idx * row_bytes >= (64ull << 20) ? 1 : 0);
     gather_rows_kernel<BYTES, R, U, MB><<<blocks, kBlock, 0, d->stream>>>(
-        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, chunk, (V*)dst, d->err_dev, stcs);
+        (const V*)src, src_rows, row_bytes / BYTES, idx, n_idx, chunk, share, (V*)dst, d->err_dev, stcs);
 }
 
 template <int BYTES>
@@ -247,6 +257,13 @@ int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
         if (v > 32) v = 32;
         return (uint32_t)(v & ~3L);
     }();
+    // Shared index lines (default on; SYNK_GATHER_SHARE=0 for A/B) need the
+    // CTA's line to fit one warp: 8 warps x chunk <= 32 indices.
+    static const int share_knob = [] {
+        const char* e = getenv("SYNK_GATHER_SHARE");
+        return e ? atoi(e) : 1;
+    }();
+    const int share = share_knob && chunk * (kBlock / 32) <= 32;
     // At most 8 CTAs of 8 warps per SM (about 2.7 waves at 3 resident
     // CTAs/SM: the oversubscription balances the random-row latency).
     // 4 rows x 2 vectors in flight per lane at <= 85 registers (3 CTAs/SM) won
@@ -257,9 +274,9 @@ int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
     const uint64_t cap = (uint64_t)d->num_sms * 8;
     if (blocks > cap) blocks = cap;
     if constexpr (BYTES == 32)  // same bytes in flight per lane as 2 x 16 B
-        launch_variant<BYTES, 4, 1, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
+        launch_variant<BYTES, 4, 1, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, share, dst);
     else
-        launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, dst);
+        launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, share, dst);
     SYNK_LAUNCHED("gather_rows_kernel");
     return SYNK_OK;
 }
