@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) gather_rows_kernel(
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
     const uint64_t stride = (((uint64_t)gridDim.x * kBlock) >> 5) * chunk;
+    // Dependents may be scheduled once every CTA has started (the last wave):
+    // a small follow-up (the call's result kernel) then waits on-chip in
+    // griddepcontrol.wait instead of paying its launch after this grid ends.
+    synk::release_dependent_grid();
     if (src_rows == 0) {  // every index is out of range
         if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)err = 1;
         return;
@@ -278,6 +282,7 @@ int launch(synk_dev* d, const void* src, uint64_t src_rows, uint64_t row_bytes,
     else
         launch_variant<BYTES, 4, 2, 3>(d, (unsigned)blocks, src, src_rows, row_bytes, idx, n_idx, chunk, share, dst);
     SYNK_LAUNCHED("gather_rows_kernel");
+    d->pdl_armed = true;
     return SYNK_OK;
 }
 
