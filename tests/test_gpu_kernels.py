@@ -157,6 +157,44 @@ def test_gather_index_list_in_pinned_host_memory(oracle):
             assert R.download(d_out, (n_idx, 256), np.float32).tobytes() == oracle.gather_rows(src, idx).tobytes()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_gather_shared_index_lines_ragged_and_bad_index(oracle, pinned):
+    """Each CTA's 8 warps share one 32-index line (gather.cu): lists that end
+    inside a line, inside a warp's 4-row chunk, or after many grid strides are
+    bit-exact, and one bad index anywhere in a line (first / last warp of a
+    line, the final partial line) raises SYNK_EBOUNDS at the next sync while
+    every other row is still gathered correctly."""
+    rng = np.random.default_rng(11)
+    src = rng.uniform(-1, 1, (3001, 64)).astype(np.float32)  # 256-byte rows: 32-byte lanes
+    with Ranks(1) as R:
+        d_src = R.upload(src)
+
+        def gather(idx):
+            d_idx = _pinned_copy(idx) if pinned else _vp(R.upload(idx))
+            d_out = R.alloc(max(len(idx), 1) * 256)
+            check(lib().synk_gather_rows(R[0], _vp(d_src), _u64(3001), _u64(256), d_idx, _u64(len(idx)),
+                                         _vp(d_out)), "gather")
+            rc = R.sync()
+            if pinned:
+                lib().synk_host_free(d_idx)
+            return rc, R.download(d_out, (len(idx), 64), np.float32)
+
+        for n_idx in (4097, 4099, 4128, 4133, 9 * 4096 + 7, 300007):
+            idx = rng.integers(0, 3001, n_idx).astype(np.uint64)
+            rc, got = gather(idx)
+            assert rc == 0 and got.tobytes() == oracle.gather_rows(src, idx).tobytes(), n_idx
+        n_idx = 4133  # 129 full lines + a partial line of 5
+        for pos in (0, 3, 28, 31, 32, 4127, 4128, 4132):
+            idx = rng.integers(0, 3001, n_idx).astype(np.uint64)
+            idx[pos] = 3001
+            rc, got = gather(idx)
+            assert rc == -1, pos  # SYNK_EBOUNDS
+            keep = np.arange(n_idx) != pos  # the bad row's content is kernel-defined (row 0 or zeros)
+            want = oracle.gather_rows(src, np.where(idx == 3001, 0, idx).astype(np.uint64))
+            assert got[keep].tobytes() == want[keep].tobytes(), pos
+        assert R.sync() == 0  # flag cleared
+
+
 def test_gather_inline_list_bit_exact(oracle):
     """synk_gather_rows_inline: a host list (pageable numpy memory) of at most
     SYNK_GATHER_INLINE_MAX indices rides in the launch as u32 kernel
