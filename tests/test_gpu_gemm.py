@@ -226,7 +226,7 @@ def test_split_k_cluster_fold_matches_planes(M, N, K, epi, tmp_path):
     assert np.load(out).tobytes() == got.tobytes()
 
 
-@pytest.mark.parametrize("rows,cols", [(64, 64), (1000, 100), (37, 5), (130, 2048)])
+@pytest.mark.parametrize("rows,cols", [(64, 64), (1000, 100), (37, 5), (130, 2048), (16, 256), (4099, 512), (8192, 2048)])
 def test_prep2_bf16_cast_and_transpose(rows, cols):
     rng = np.random.default_rng(rows * cols)
     x = rng.uniform(-3, 3, (rows, cols)).astype(np.float32)
