@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(NT, 2)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     constexpr int kBK = 128 / (KIND == 0 ? 2 : 4);  // elements per 128-byte K block
+    // PDL: the next GEMM on the stream may be scheduled as soon as every CTA
+    // of this one runs; it waits (below) before touching global memory.
+    synk::release_dependent_grid();
     // split-K (gridDim.z > 1): CTA z owns K blocks [kb0, kb0 + num_kb) and
     // stores its raw fp32 partial to plane z of C (host folds the planes).
     const int kb0 = (int)(blockIdx.z * kb_per);
@@ -236,6 +239,9 @@ __global__ void __launch_bounds__(NT, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // Launched programmatically after the previous kernel (PDL): barriers and
+    // TMEM are set up while it drains; no global access before it completed.
+    synk::wait_prerequisite_grid();
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
@@ -625,6 +631,7 @@ __global__ void __launch_bounds__(PThreads, 1)
     const uint32_t rank = PAIR == 2 ? cluster_rank() : 0u;
     const bool leader = rank == 0;
     const uint32_t unit = blockIdx.x / PAIR, units = gridDim.x / PAIR;  // pair (or CTA) index / count
+    synk::release_dependent_grid();  // PDL: see gemm_tc_kernel
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     constexpr int kBK = 64;  // bf16 elements per 128-byte K block
@@ -669,6 +676,7 @@ __global__ void __launch_bounds__(PThreads, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    synk::wait_prerequisite_grid();  // PDL: prologue overlapped the previous kernel's tail
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer (both CTAs: this CTA's A rows and B rows) ----
@@ -923,6 +931,18 @@ int make_map_mn(CUtensorMap* map, const void* base, uint64_t k_rows, uint64_t mn
 
 constexpr size_t kSmemBytes = 2 * kStages * kTileBytes + 1024 /*align*/ + 256 /*barriers*/;
 
+// Programmatic dependent launch between back-to-back tcgen05 GEMMs: each one
+// releases its dependents at CTA entry and waits (griddepcontrol.wait) after
+// its barrier / TMEM prologue, so the next GEMM's launch and prologue overlap
+// this one's tail. SYNK_GEMM_PDL=0 launches them plainly (A/B).
+bool pdl_gemm() {
+    static const bool on = [] {
+        const char* e = getenv("SYNK_GEMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int KIND>
 int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
            const CUtensorMap& b1, uint64_t M, uint64_t N, uint64_t K, const EpiArgs& e, uint32_t splits = 1,
@@ -944,15 +964,18 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
         cfg.blockDim = dim3(wide ? 256 : 128);
         cfg.dynamicSmemBytes = kSmemBytes;
         cfg.stream = d->stream;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 1;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = splits;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = pdl_gemm() && d->pdl_armed ? 2 : 1;
         SYNK_CU(cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, passes, (uint32_t)M, (uint32_t)N, (uint32_t)K, e, kb_per,
                                    layout, 1, n_eff));
+        d->pdl_armed = pdl_gemm();
         return SYNK_OK;
     }
     if (wide) {
@@ -967,6 +990,7 @@ int launch(synk_dev* d, int passes, const CUtensorMap& a0, const CUtensorMap& a1
                                                                        (uint32_t)K, e, kb_per, layout, 0, n_eff);
     }
     SYNK_LAUNCHED("gemm_tc_kernel");
+    d->pdl_armed = pdl_gemm();
     return SYNK_OK;
 }
 
@@ -1248,19 +1272,22 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
             cfg.blockDim = dim3(PThreads);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = d->stream;
-            cudaLaunchAttribute attr[1];
+            cudaLaunchAttribute attr[2];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = 2;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
-            cfg.numAttrs = 1;
+            cfg.numAttrs = pdl_gemm() && d->pdl_armed ? 2 : 1;  // PDL after a kernel that released at entry
             if (act_tma)
                 SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2, true>, a0, bw, ta, (uint32_t)M,
                                            (uint32_t)N, (uint32_t)K, e, lay));
             else
                 SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_tc_persistent_kernel<2, false>, a0, bw, ta, (uint32_t)M,
                                            (uint32_t)N, (uint32_t)K, e, lay));
+            d->pdl_armed = pdl_gemm();
             return SYNK_OK;
         }
         constexpr size_t smem = PCfg<1>::kSmem;
@@ -1271,6 +1298,7 @@ int synk_gemm_tc2(synk_dev* d, int kind, uint64_t M, uint64_t N, uint64_t K, con
         gemm_tc_persistent_kernel<1, false><<<grid, PThreads, smem, d->stream>>>(a0, bw, bw, (uint32_t)M, (uint32_t)N,
                                                                                    (uint32_t)K, e, lay);
         SYNK_LAUNCHED("gemm_tc_persistent_kernel");
+        d->pdl_armed = pdl_gemm();
         return SYNK_OK;
     }
     // Narrow N (one column tile) with a K-major B: UMMA N = N rounded up to 16
