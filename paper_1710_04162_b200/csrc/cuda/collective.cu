@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kStepBlock) allreduce_step_kernel(
     Ptrs params, Ptrs grads, Ptrs aux0, Ptrs aux1, int world, int rank, int grad_op,
     double inv_w, synk::RuleParams rp, int naux, bool coherent, bool grads_local, uint64_t lo, uint64_t hi,
     int vec_bytes, Shadow sh) {
+    synk::wait_prerequisite_grid();  // no-op unless launched as a follow-up (W = 1, after a GEMM)
     const int fop = grad_op == SYNK_OP_MEAN ? SYNK_OP_SUM : grad_op;
     uint64_t tid = (uint64_t)blockIdx.x * kStepBlock + threadIdx.x;
     uint64_t stride = (uint64_t)gridDim.x * kStepBlock;
@@ -571,15 +572,25 @@ int allreduce_step_t(synk_dev* d, int w, int grad_op, const synk::RuleParams& rp
                 return rc;                                                                                       \
             if (!(flags & SYNK_STEP_BACKGROUND))                                                                 \
                 grid = synk::resident_grid((const void*)allreduce_step_kernel<T, WW, true>, d->device, kStepBlock, items); \
-            allreduce_step_kernel<T, WW, true><<<grid, kStepBlock, 0, d->stream>>>(                                  \
-                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
+            if (WW == 1) /* one GPU: programmatically dependent on the weight-gradient product */              \
+                SYNK_CU(synk::launch_follow_up(d, allreduce_step_kernel<T, WW, true>, grid, kStepBlock, P, G, A0, A1, w, \
+                                               d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi,      \
+                                               vec_bytes, S));                                                        \
+            else                                                                                                 \
+                allreduce_step_kernel<T, WW, true><<<grid, kStepBlock, 0, d->stream>>>(                              \
+                    P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);         \
         } else {                                                                                                 \
             if (int rc = synk::prefer_shared_carveout((const void*)allreduce_step_kernel<T, WW, false>, d->device); rc) \
                 return rc;                                                                                       \
             if (!(flags & SYNK_STEP_BACKGROUND))                                                                 \
                 grid = synk::resident_grid((const void*)allreduce_step_kernel<T, WW, false>, d->device, kStepBlock, items); \
-            allreduce_step_kernel<T, WW, false><<<grid, kStepBlock, 0, d->stream>>>(                                 \
-                P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);             \
+            if (WW == 1)                                                                                         \
+                SYNK_CU(synk::launch_follow_up(d, allreduce_step_kernel<T, WW, false>, grid, kStepBlock, P, G, A0, A1, w, \
+                                               d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi,      \
+                                               vec_bytes, S));                                                        \
+            else                                                                                                 \
+                allreduce_step_kernel<T, WW, false><<<grid, kStepBlock, 0, d->stream>>>(                             \
+                    P, G, A0, A1, w, d->rank, grad_op, inv_w, rp, naux, coherent, grads_local, lo, hi, vec_bytes, S);         \
         }                                                                                                        \
         break;
         SYNK_ARS_CASE(1) SYNK_ARS_CASE(2) SYNK_ARS_CASE(3) SYNK_ARS_CASE(4)

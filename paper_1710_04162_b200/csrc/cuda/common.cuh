@@ -70,6 +70,22 @@ cudaError_t launch_follow_up(synk_dev* d, void (*kernel)(KArgs...), unsigned gri
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// The same for a 2-D grid.
+template <class... KArgs, class... Args>
+cudaError_t launch_follow_up_2d(synk_dev* d, void (*kernel)(KArgs...), dim3 grid, unsigned block, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.stream = d->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = d->pdl_armed ? 1 : 0;
+    d->pdl_armed = false;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ void wait_prerequisite_grid() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void release_dependent_grid() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -590,6 +590,10 @@ __global__ void __launch_bounds__(256) loss_delta_bf16_kernel(const float* __res
     __shared__ __nv_bfloat16 tile[kLossTileC][kLossTileR + 2];
     __shared__ double red[256];
     __shared__ int last;
+    // PDL: launched programmatically after the forward GEMM (waits for it
+    // before any global access) and releases the backward GEMM behind it.
+    synk::release_dependent_grid();
+    synk::wait_prerequisite_grid();
     const uint64_t r0 = (uint64_t)blockIdx.y * kLossTileR, c0 = (uint64_t)blockIdx.x * kLossTileC;
     const int tc = threadIdx.x % kLossTileC, tr = threadIdx.x / kLossTileC;  // 64 x 4
     double s = 0.0;
@@ -798,10 +802,12 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         const dim3 grid((unsigned)((dl + kLossTileC - 1) / kLossTileC), (unsigned)((n + kLossTileR - 1) / kLossTileR));
         SYNK_REQUIRE((uint64_t)grid.x * grid.y <= kLossBlocks * 8, SYNK_EARG, "mlp: loss tile grid too large");
         if (int rc = synk::prefer_shared_carveout((const void*)loss_delta_bf16_kernel, d->device); rc) return rc;
-        loss_delta_bf16_kernel<<<grid, 256, 0, d->stream>>>(
-            pred, y, n, dl, inv_n, bf(B.off_d[L]), pad8(dims[L]), narrow(L) ? bf(B.off_dT[L]) : nullptr, pad8(n),
-            partial, reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n, loss, rows);
+        SYNK_CU(synk::launch_follow_up_2d(
+            d, loss_delta_bf16_kernel, grid, 256, pred, y, n, dl, inv_n, bf(B.off_d[L]), pad8(dims[L]),
+            narrow(L) ? bf(B.off_dT[L]) : nullptr, pad8(n), partial, reinterpret_cast<unsigned*>(d->flags_dev + 3),
+            0.5 * inv_n, loss, rows));
         SYNK_LAUNCHED("loss_delta_bf16_kernel");
+        d->pdl_armed = true;
     }
 
     // backward: every dX product first (they read the bf16 W_l, which no
