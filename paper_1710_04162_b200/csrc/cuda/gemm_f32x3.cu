@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     uint64_t* tempty = tfull + 2;            // [2]
     uint64_t* act_full = tempty + 2;         // [1]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_full + 1);
+    synk::release_dependent_grid();  // PDL: the next product may be scheduled (it waits below)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    synk::wait_prerequisite_grid();  // PDL: prologue overlapped the previous kernel; no global access before
 
     float acc[BN];
 #pragma unroll
@@ -404,6 +406,7 @@ struct SplitBatch {
 // split tile, the blocks after it set the constant rows (one row each).
 __global__ void __launch_bounds__(256) tf32_stage_kernel(SplitBatch batch, synk_tf32_rows fill) {
     __shared__ float tile[32][33];
+    synk::release_dependent_grid();  // PDL: the first product may be scheduled behind it
     const uint32_t b = blockIdx.x;
     if (b >= batch.first[batch.count]) {
         const uint32_t i = b - batch.first[batch.count];
@@ -442,6 +445,17 @@ uint32_t choose_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int ctas_per_
     return (uint32_t)((num_kb + per - 1) / per);
 }
 
+// Programmatic dependent launch along the C1 chain (stage -> products ->
+// loss -> products): each kernel releases its dependents at entry and waits
+// after its prologue. SYNK_F32X3_PDL=0 launches plainly (A/B).
+bool pdl_f32x3() {
+    static const bool on = [] {
+        const char* e = getenv("SYNK_F32X3_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int BN, int EK>
 int launch_f32x3(synk_dev* d, const CUtensorMap& ah, const CUtensorMap& al, const void* b_hi, const void* b_lo,
                  uint64_t ldb, uint64_t M, uint64_t N, uint64_t K, const Out& o) {
@@ -465,15 +479,18 @@ int launch_f32x3(synk_dev* d, const CUtensorMap& ah, const CUtensorMap& al, cons
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = d->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = S;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_f32x3() && d->pdl_armed ? 2 : 1;  // PDL after a kernel that released at entry
     SYNK_CU(cudaLaunchKernelEx(&cfg, gemm_f32x3_kernel<BN, EK>, ah, al, bh, bl, ta, act_tma, (uint32_t)M, (uint32_t)N,
                                (uint32_t)K, kb_per, o));
+    d->pdl_armed = pdl_f32x3();
     return SYNK_OK;
 }
 
@@ -541,6 +558,7 @@ int synk_tf32_stage(synk_dev* d, const synk_tf32_job* jobs, uint32_t count, cons
     synk::DeviceGuard g(d->device);
     tf32_stage_kernel<<<blocks + rows.count, 256, 0, d->stream>>>(batch, rows);
     SYNK_LAUNCHED("tf32_stage_kernel");
+    d->pdl_armed = pdl_f32x3();
     return SYNK_OK;
 }
 

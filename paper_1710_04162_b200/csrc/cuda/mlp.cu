@@ -223,6 +223,8 @@ __global__ void __launch_bounds__(kThreads) loss_delta_kernel(const T* __restric
                                                               uint64_t ycols = 1, DeltaSplit ds = {}) {
     __shared__ double red[kThreads];
     __shared__ int last;
+    synk::release_dependent_grid();  // PDL: the backward product behind it may be scheduled
+    synk::wait_prerequisite_grid();  // launched as a follow-up of the last forward product
     double s = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n_el;
          i += (uint64_t)gridDim.x * kThreads) {
@@ -353,10 +355,11 @@ int loss_grad_t(synk_dev* d, const uint64_t* dims, uint32_t layers, const Plan& 
     if (blocks > kLossBlocks) blocks = kLossBlocks;
     if (blocks < 1) blocks = 1;
     double inv_n = 1.0 / (double)n;
-    loss_delta_kernel<T><<<blocks, kThreads, 0, d->stream>>>(acts[layers], y, n_el, inv_n, dA, partial,
-                                                             reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n,
-                                                             loss, rows, dims[layers]);
+    SYNK_CU(synk::launch_follow_up(d, loss_delta_kernel<T>, (unsigned)blocks, kThreads, acts[layers], y, n_el, inv_n,
+                                   dA, partial, reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n, loss, rows,
+                                   dims[layers], DeltaSplit{}));
     SYNK_LAUNCHED("loss_delta_kernel");
+    d->pdl_armed = true;
 
     T* delta = dA;
     T* spare = dB;
@@ -491,13 +494,12 @@ int loss_grad_f32tc(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P
     const uint64_t n_el = n * dims[L];
     const int blocks = (int)std::min<uint64_t>(kLossBlocks, std::max<uint64_t>(1, (n_el + kThreads - 1) / kThreads));
     const double inv_n = 1.0 / (double)n;
-    loss_delta_kernel<float><<<blocks, kThreads, 0, d->stream>>>(F(T.act[L]), y, n_el, inv_n, F(T.delta),
-                                                                 reinterpret_cast<double*>(base + T.partial),
-                                                                 reinterpret_cast<unsigned*>(d->flags_dev + 3),
-                                                                 0.5 * inv_n, loss, rows, dims[L],
-                                                                 DeltaSplit{L >= 2 ? F(T.dh[0]) : nullptr,
-                                                                            L >= 2 ? F(T.dl[0]) : nullptr, pad4(dims[L]),
-                                                                            F(T.dth[0]), F(T.dtl[0]), pn});
+    SYNK_CU(synk::launch_follow_up(d, loss_delta_kernel<float>, (unsigned)blocks, kThreads, F(T.act[L]), y, n_el, inv_n,
+                                   F(T.delta), reinterpret_cast<double*>(base + T.partial),
+                                   reinterpret_cast<unsigned*>(d->flags_dev + 3), 0.5 * inv_n, loss, rows, dims[L],
+                                   DeltaSplit{L >= 2 ? F(T.dh[0]) : nullptr, L >= 2 ? F(T.dl[0]) : nullptr,
+                                              pad4(dims[L]), F(T.dth[0]), F(T.dtl[0]), pn}));
+    d->pdl_armed = true;
     SYNK_LAUNCHED("loss_delta_kernel");
     int cur = 0;
     for (uint32_t l = L; l-- > 0;) {
@@ -903,6 +905,7 @@ int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
             e.used = ++gc.clock;
             gc.misses_in_a_row = 0;
             SYNK_CU(cudaGraphLaunch(e.exec, d->stream));
+            d->pdl_armed = false;  // a graph is not a kernel that released its dependents
             return SYNK_OK;
         }
     if (++gc.misses_in_a_row > GraphCache::kGiveUp) {
@@ -918,6 +921,7 @@ int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
                 d->rank, gc.entries.size(), gc.misses_in_a_row, key.ptrs[0], key.ptrs[1], key.ptrs[2], key.ptrs[3],
                 key.ptrs[4], key.ptrs[5], key.ptrs[6]);
     cudaGraph_t graph = nullptr;
+    d->pdl_armed = false;  // no programmatic edge onto work outside the graph
     SYNK_CU(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal));
     const int rc = launch_all();
     const cudaError_t ec = cudaStreamEndCapture(d->stream, &graph);
@@ -941,6 +945,7 @@ int graph_launch(synk_dev* d, const GraphKey& key, F&& launch_all) {
     }
     gc.entries.push_back({key, exec, ++gc.clock});
     SYNK_CU(cudaGraphLaunch(exec, d->stream));
+    d->pdl_armed = false;
     return SYNK_OK;
 }
 
