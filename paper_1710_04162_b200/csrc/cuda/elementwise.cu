@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(D* __restrict__ dst, const
 }
 
 int read_flag(synk_dev* d, int* out) {
+    d->pdl_armed = false;
     SYNK_CU(cudaMemcpyAsync(d->flags_host + 1, d->flags_dev + 1, sizeof(int),
                             cudaMemcpyDeviceToHost, d->stream));
     SYNK_CU(cudaStreamSynchronize(d->stream));
@@ -562,6 +563,7 @@ int synk_cast(synk_dev* d, int dst_dtype, void* dst, int src_dtype, const void* 
     if (n == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
     if (dst_dtype == src_dtype) {
+        d->pdl_armed = false;
         SYNK_CU(cudaMemcpyAsync(dst, src, n * synk::dtype_bytes(src_dtype), cudaMemcpyDefault, d->stream));
         return SYNK_OK;
     }
@@ -578,6 +580,7 @@ int synk_equal(synk_dev* d, const void* a, const void* b, uint64_t bytes, int* e
     *equal = 1;
     if (bytes == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
+    d->pdl_armed = false;
     SYNK_CU(cudaMemsetAsync(d->flags_dev + 1, 0, sizeof(int), d->stream));
     if (aligned16(a, b) && bytes % 16 == 0) {
         uint64_t n = bytes / 16;
@@ -599,6 +602,7 @@ int synk_all_finite(synk_dev* d, int dtype, const void* x, uint64_t n, int* fini
     *finite = 1;
     if (n == 0) return SYNK_OK;
     synk::DeviceGuard g(d->device);
+    d->pdl_armed = false;
     SYNK_CU(cudaMemsetAsync(d->flags_dev + 1, 0, sizeof(int), d->stream));
     unsigned grid = synk::grid_for(d, n, kBlock);
     if (dtype == SYNK_F32)

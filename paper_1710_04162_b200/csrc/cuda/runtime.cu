@@ -249,6 +249,7 @@ int synk_wait_peer_slot(synk_dev* d, const synk_dev* peer, int slot) {
     SYNK_REQUIRE(slot >= 0 && slot < 64, SYNK_EARG, "synk_wait_peer_slot: slot out of range");
     SYNK_REQUIRE(peer && peer->ready[slot], SYNK_EARG, "synk_wait_peer: the peer has not signalled");
     DeviceGuard g(d->device);
+    d->pdl_armed = false;  // programmatic launches only directly behind a kernel
     SYNK_CU(cudaStreamWaitEvent(d->stream, peer->ready[slot], 0));
     return SYNK_OK;
 }
@@ -414,6 +415,7 @@ int synk_host_device_ptr(const void* host, const void** dev_ptr) {
 int synk_copy(synk_dev* d, void* dst, const void* src, uint64_t bytes) {
     if (bytes == 0) return SYNK_OK;
     DeviceGuard g(d->device);
+    d->pdl_armed = false;  // programmatic launches only directly behind a kernel
     SYNK_CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, d->stream));
     return SYNK_OK;
 }
@@ -422,6 +424,7 @@ int synk_copy2d(synk_dev* d, void* dst, uint64_t dpitch, const void* src, uint64
                 uint64_t row_bytes, uint64_t rows) {
     if (rows == 0 || row_bytes == 0) return SYNK_OK;
     DeviceGuard g(d->device);
+    d->pdl_armed = false;
     SYNK_CU(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyDefault,
                               d->stream));
     return SYNK_OK;
@@ -430,6 +433,7 @@ int synk_copy2d(synk_dev* d, void* dst, uint64_t dpitch, const void* src, uint64
 int synk_memset(synk_dev* d, void* dst, int value, uint64_t bytes) {
     if (bytes == 0) return SYNK_OK;
     DeviceGuard g(d->device);
+    d->pdl_armed = false;  // programmatic launches only directly behind a kernel
     SYNK_CU(cudaMemsetAsync(dst, value, bytes, d->stream));
     return SYNK_OK;
 }
