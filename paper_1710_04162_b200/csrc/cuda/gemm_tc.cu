@@ -1067,6 +1067,7 @@ __global__ void __launch_bounds__(256) prep2_bf16_kernel(const float* __restrict
     // rowmap != nullptr: output row r is input row rowmap[r] (index-fused
     // gather: the batch is read straight from the whole source).
     __shared__ float tile[64][65];
+    synk::release_dependent_grid();  // PDL: the first forward GEMM may be scheduled behind it
     __shared__ uint64_t srow[64];
     const uint64_t r0 = (uint64_t)blockIdx.y * 64, c0 = (uint64_t)blockIdx.x * 64;
     const int t = threadIdx.x;
@@ -1181,6 +1182,7 @@ int synk_gemm_prep2_bf16_rows(synk_dev* d, const float* in, const uint64_t* rowm
     prep2_bf16_kernel<<<grid, 256, 0, d->stream>>>(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out), ld_out,
                                                    static_cast<__nv_bfloat16*>(out_t), ld_out_t, vec_in, rowmap);
     SYNK_LAUNCHED("prep2_bf16_kernel");
+    d->pdl_armed = true;
     return SYNK_OK;
 }
 

@@ -757,6 +757,17 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
         rows_waited = true;
         return synk_wait_peer_slot(d, opts->rows_ready_on, opts->rows_ready_slot);
     };
+    // the constant ones rows of every a_l^T first: they do not need the index
+    // list, so they run while its stage copy is still in flight
+    {
+        OnesRows o{};
+        o.count = L;
+        for (uint32_t l = 0; l < L; ++l) o.p[l] = bf(B.off_actT[l]) + dims[l] * pad8(n);
+        if (int rc = synk::prefer_shared_carveout((const void*)ones_rows_kernel, d->device); rc) return rc;
+        if (int rc = synk::prefer_shared_carveout((const void*)loss_delta_kernel<float>, d->device); rc) return rc;
+        ones_rows_kernel<<<dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 64), L), 256, 0, d->stream>>>(o, n);
+        SYNK_LAUNCHED("ones_rows_kernel");
+    }
     // The x staging reads the HBM copy of the list: read in place over PCIe
     // (rows_host) every 64x64 tile re-fetched its 64 indices at PCIe latency,
     // 121 us instead of 27 us for the C5 batch (profiles/r02_c5_trace.txt),
@@ -769,15 +780,6 @@ int loss_grad_bf16(synk_dev* d, const uint64_t* dims, uint32_t L, const Plan& P,
                                            bf(B.off_actT[0]), pad8(n));
         rc)
         return rc;
-    {
-        OnesRows o{};
-        o.count = L;
-        for (uint32_t l = 0; l < L; ++l) o.p[l] = bf(B.off_actT[l]) + dims[l] * pad8(n);
-        if (int rc = synk::prefer_shared_carveout((const void*)ones_rows_kernel, d->device); rc) return rc;
-        if (int rc = synk::prefer_shared_carveout((const void*)loss_delta_kernel<float>, d->device); rc) return rc;
-        ones_rows_kernel<<<dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 64), L), 256, 0, d->stream>>>(o, n);
-        SYNK_LAUNCHED("ones_rows_kernel");
-    }
 
     // forward
     float* pred = reinterpret_cast<float*>(base + B.off_pred);
